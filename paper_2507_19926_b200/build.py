@@ -1,0 +1,95 @@
+"""Build the CUDA extension in-tree: codegen + nvcc (sm_100a) -> libtilemedian_b200.so.
+
+    python -m paper_2507_19926_b200.build [-j N] [--force]
+
+Object files go to ``paper_2507_19926_b200/_build/``; the shared library to
+``paper_2507_19926_b200/libtilemedian_b200.so`` (git-ignored, shipped to the GPU
+box by gpurun).  ``-Xptxas -v`` output (registers, spills, shared memory) is
+kept in ``_build/ptxas.log``.
+"""
+from __future__ import annotations
+
+import argparse
+import concurrent.futures as cf
+import glob
+import os
+import subprocess
+import sys
+
+from . import codegen
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(PKG, "csrc")
+BUILD = os.path.join(PKG, "_build")
+LIB = os.path.join(PKG, "libtilemedian_b200.so")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
+         "--expt-relaxed-constexpr"]
+
+
+def _sources() -> list[str]:
+    return sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "gen", "*.cu")))
+
+
+def _headers() -> list[str]:
+    return sorted(glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h"))
+                  + glob.glob(os.path.join(CSRC, "gen", "*.cuh"))
+                  + glob.glob(os.path.join(CSRC, "gen", "*.inc"))
+                  + glob.glob(os.path.join(PKG, "..", "include", "*.h")))
+
+
+def _obj(src: str) -> str:
+    rel = os.path.relpath(src, CSRC).replace(os.sep, "_")
+    return os.path.join(BUILD, rel[:-3] + ".o")
+
+
+def _compile(src: str) -> tuple[str, str]:
+    obj = _obj(src)
+    cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+    p = subprocess.run(cmd, capture_output=True, text=True)
+    if p.returncode != 0:
+        raise RuntimeError(f"nvcc failed for {src}:\n{p.stderr[-6000:]}")
+    return src, p.stderr
+
+
+def build(jobs: int | None = None, force: bool = False, verbose: bool = False) -> str:
+    codegen.generate()
+    os.makedirs(BUILD, exist_ok=True)
+    newest_hdr = max((os.path.getmtime(h) for h in _headers()), default=0)
+    todo = []
+    for src in _sources():
+        obj = _obj(src)
+        if (force or not os.path.exists(obj) or os.path.getmtime(obj) < os.path.getmtime(src)
+                or os.path.getmtime(obj) < newest_hdr):
+            todo.append(src)
+    logs = {}
+    if todo:
+        jobs = jobs or min(len(todo), os.cpu_count() or 4)
+        with cf.ThreadPoolExecutor(jobs) as pool:
+            for src, log in pool.map(_compile, todo):
+                logs[src] = log
+                if verbose:
+                    print(f"compiled {os.path.relpath(src, PKG)}", file=sys.stderr)
+        with open(os.path.join(BUILD, "ptxas.log"), "a") as f:
+            for src, log in logs.items():
+                f.write(f"==== {src}\n{log}\n")
+    objs = [_obj(s) for s in _sources()]
+    if todo or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
+        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart"]
+        p = subprocess.run(cmd, capture_output=True, text=True)
+        if p.returncode != 0:
+            raise RuntimeError(f"link failed:\n{p.stderr[-4000:]}")
+    return LIB
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("-j", type=int, default=None)
+    ap.add_argument("--force", action="store_true")
+    a = ap.parse_args()
+    print(build(a.j, a.force, verbose=True))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,201 @@
+// tm_api.cu -- the C ABI (include/tilemedian_b200.h): validation, dispatch,
+// launch accounting and the host-buffer entry point.
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "../../include/tilemedian_b200.h"
+#include "tm_kernels.h"
+
+namespace tmb {
+#include "gen/dispatch.inc"
+}
+
+namespace {
+
+thread_local char g_err[512] = "";
+std::atomic<int64_t> g_launches{0};
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+const tmb::OblEntry* find_obl(int bits, int k) {
+  for (const auto& e : tmb::kOblTable)
+    if (e.bits == bits && e.k == k) return &e;
+  return nullptr;
+}
+
+// Kernel routing.  Results are identical whichever exact kernel runs; the
+// variant only chooses the algorithm (engine.py:36-52).
+int route(int bits, int kw, int kh, int variant) {
+  const bool square = kw == kh;
+  const bool obl = square && find_obl(bits, kw) != nullptr;
+  switch (variant) {
+    case TM_VARIANT_ORACLE:
+      return TM_KERNEL_SELECT;
+    case TM_VARIANT_OBLIVIOUS:
+      return obl ? TM_KERNEL_OBLIVIOUS : TM_KERNEL_SELECT;
+    case TM_VARIANT_AWARE:
+      return TM_KERNEL_SELECT;
+    default:  // auto
+      return obl ? TM_KERNEL_OBLIVIOUS : TM_KERNEL_SELECT;
+  }
+}
+
+int check_common(int width, int rows, int bits, int kw, int kh, int variant) {
+  if (bits != 8 && bits != 16 && bits != 32)
+    return fail(TM_ETYPE, "unsupported element width %d bits (expected 8, 16 or 32)", bits);
+  if (width < 1 || rows < 1)
+    return fail(TM_EINVAL, "expected a non-empty 2-D image, got %dx%d", width, rows);
+  if (kw < 3 || kh < 3 || !(kw & 1) || !(kh & 1))
+    return fail(TM_EINVAL, "kernel sides must be odd and >= 3, got %dx%d", kw, kh);
+  if (kw > 127 || kh > 127)
+    return fail(TM_EINVAL, "kernel sides above 127 are not supported, got %dx%d", kw, kh);
+  if (variant < TM_VARIANT_AUTO || variant > TM_VARIANT_ORACLE)
+    return fail(TM_EINVAL, "unknown variant %d", variant);
+  return TM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tm_median2d_band(const void* src, int64_t src_pitch, int32_t src_rows, int32_t out_row0,
+                     int32_t out_rows, void* dst, int64_t dst_pitch, int32_t width,
+                     int32_t channels, int32_t bits, int32_t k_w, int32_t k_h,
+                     int32_t variant, void* stream) {
+  int rc = check_common(width, src_rows, bits, k_w, k_h, variant);
+  if (rc) return rc;
+  if (!src || !dst) return fail(TM_EINVAL, "null buffer");
+  if (channels < 1 || channels > 65535) return fail(TM_EINVAL, "bad channel count %d", channels);
+  const int esz = bits / 8;
+  if (out_row0 < 0 || out_rows < 0 || out_row0 + out_rows > src_rows)
+    return fail(TM_EINVAL, "output rows [%d, %d) outside source rows [0, %d)", out_row0,
+                out_row0 + out_rows, src_rows);
+  if (src_pitch % esz || dst_pitch % esz)
+    return fail(TM_EINVAL, "pitches must be multiples of the element size");
+  if (src_pitch < (int64_t)width * channels * esz || dst_pitch < (int64_t)width * channels * esz)
+    return fail(TM_EINVAL, "pitch smaller than a row");
+  if (out_rows == 0) return TM_OK;
+  tmb::Job job;
+  job.src = src;
+  job.dst = dst;
+  job.src_pitch = src_pitch / esz;
+  job.dst_pitch = dst_pitch / esz;
+  job.width = width;
+  job.src_h = src_rows;
+  job.out_y0 = out_row0;
+  job.out_h = out_rows;
+  job.channels = channels;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int err;
+  switch (route(bits, k_w, k_h, variant)) {
+    case TM_KERNEL_OBLIVIOUS:
+      err = find_obl(bits, k_w)->fn(job, s);
+      break;
+    default:
+      err = tmb::launch_select(bits, job, k_w, k_h, s);
+      break;
+  }
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (err != cudaSuccess)
+    return fail(TM_ECUDA, "CUDA launch failed: %s", cudaGetErrorString((cudaError_t)err));
+  return TM_OK;
+}
+
+int tm_median2d_rect(const void* src, int64_t src_pitch, void* dst, int64_t dst_pitch,
+                     int32_t width, int32_t height, int32_t bits, int32_t k_w, int32_t k_h,
+                     int32_t variant, void* stream) {
+  return tm_median2d_band(src, src_pitch, height, 0, height, dst, dst_pitch, width, 1, bits, k_w,
+                          k_h, variant, stream);
+}
+
+int tm_median2d(const void* src, int64_t src_pitch, void* dst, int64_t dst_pitch, int32_t width,
+                int32_t height, int32_t bits, int32_t k, int32_t variant, void* stream) {
+  return tm_median2d_band(src, src_pitch, height, 0, height, dst, dst_pitch, width, 1, bits, k, k,
+                          variant, stream);
+}
+
+int tm_median2d_planes(const void* src, int64_t src_pitch, void* dst, int64_t dst_pitch,
+                       int32_t width, int32_t height, int32_t channels, int32_t bits, int32_t k,
+                       int32_t variant, void* stream) {
+  return tm_median2d_band(src, src_pitch, height, 0, height, dst, dst_pitch, width, channels, bits,
+                          k, k, variant, stream);
+}
+
+int tm_median2d_host(const void* src, int64_t src_pitch, void* dst, int64_t dst_pitch,
+                     int32_t width, int32_t height, int32_t channels, int32_t bits, int32_t k_w,
+                     int32_t k_h, int32_t variant, int32_t device) {
+  int rc = check_common(width, height, bits, k_w, k_h, variant);
+  if (rc) return rc;
+  if (!src || !dst) return fail(TM_EINVAL, "null buffer");
+  if (channels < 1) return fail(TM_EINVAL, "bad channel count %d", channels);
+  const int64_t row = (int64_t)width * channels * (bits / 8);
+  if (src_pitch < row || dst_pitch < row) return fail(TM_EINVAL, "pitch smaller than a row");
+  struct Scratch {
+    void* buf = nullptr;
+    size_t bytes = 0;
+    cudaStream_t stream = nullptr;
+  };
+  static thread_local std::vector<Scratch> per_dev;
+  if (device < 0) return fail(TM_EINVAL, "bad device %d", device);
+  if ((int)per_dev.size() <= device) per_dev.resize(device + 1);
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return fail(TM_ECUDA, "cudaSetDevice: %s", cudaGetErrorString(e));
+  Scratch& sc = per_dev[device];
+  const size_t need = 2 * (size_t)row * height;
+  if (sc.bytes < need) {
+    if (sc.buf) cudaFree(sc.buf);
+    sc.buf = nullptr;
+    sc.bytes = 0;
+    e = cudaMalloc(&sc.buf, need);
+    if (e != cudaSuccess) return fail(TM_ECUDA, "cudaMalloc: %s", cudaGetErrorString(e));
+    sc.bytes = need;
+  }
+  if (!sc.stream) {
+    e = cudaStreamCreateWithFlags(&sc.stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return fail(TM_ECUDA, "cudaStreamCreate: %s", cudaGetErrorString(e));
+  }
+  char* din = static_cast<char*>(sc.buf);
+  char* dout = din + (size_t)row * height;
+  e = cudaMemcpy2DAsync(din, row, src, src_pitch, row, height, cudaMemcpyHostToDevice, sc.stream);
+  if (e != cudaSuccess) return fail(TM_ECUDA, "H2D copy: %s", cudaGetErrorString(e));
+  rc = tm_median2d_band(din, row, height, 0, height, dout, row, width, channels, bits, k_w, k_h,
+                        variant, sc.stream);
+  if (rc) return rc;
+  e = cudaMemcpy2DAsync(dst, dst_pitch, dout, row, row, height, cudaMemcpyDeviceToHost, sc.stream);
+  if (e != cudaSuccess) return fail(TM_ECUDA, "D2H copy: %s", cudaGetErrorString(e));
+  e = cudaStreamSynchronize(sc.stream);
+  if (e != cudaSuccess) return fail(TM_ECUDA, "kernel failed: %s", cudaGetErrorString(e));
+  return TM_OK;
+}
+
+int tm_dispatch_query(int32_t bits, int32_t k_w, int32_t k_h, int32_t variant) {
+  if (check_common(1, 1, bits, k_w, k_h, variant)) return TM_KERNEL_NONE;
+  return route(bits, k_w, k_h, variant);
+}
+
+const char* tm_kernel_name(int32_t kernel) {
+  switch (kernel) {
+    case TM_KERNEL_OBLIVIOUS: return "oblivious";
+    case TM_KERNEL_AWARE: return "aware";
+    case TM_KERNEL_SELECT: return "select";
+    default: return "none";
+  }
+}
+
+int64_t tm_launch_count(void) { return g_launches.load(); }
+
+const char* tm_last_error(void) { return g_err; }
+
+const char* tm_version(void) { return "tilemedian_b200 0.1.0 (sm_100a)"; }
+
+}  // extern "C"

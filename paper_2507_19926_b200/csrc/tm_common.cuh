@@ -1,0 +1,93 @@
+// tm_common.cuh -- shared helpers of the sm_100a median kernels.
+//
+// Lane model.  Every median kernel works on 32-bit "lane words":
+//   * 8- and 16-bit images: two independent problems packed as u16x2 -- the
+//     low half-word belongs to lane 0, the high half-word to lane 1.  min/max
+//     compile to VIMNMX.U16x2 / VIMNMX3.U16x2 (native on sm_100a, one
+//     instruction for two selections);
+//   * 32-bit images: one problem per word, VIMNMX.U32 / VIMNMX3.U32.
+// 8-bit data is widened to 16-bit lanes (sm_100a has no native u8x4 min/max:
+// __vminu4 lowers to LOP3/PRMT sequences -- profiles/r01_minmax_microbench.txt).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tmb {
+
+template <typename T>
+struct Lanes;
+
+template <>
+struct Lanes<uint8_t> {
+  static constexpr int kLanes = 2;
+  __device__ __forceinline__ static uint32_t mn(uint32_t a, uint32_t b) { return __vminu2(a, b); }
+  __device__ __forceinline__ static uint32_t mx(uint32_t a, uint32_t b) { return __vmaxu2(a, b); }
+  __device__ __forceinline__ static uint32_t pack(uint8_t lo, uint8_t hi) {
+    return (uint32_t)lo | ((uint32_t)hi << 16);
+  }
+  __device__ __forceinline__ static uint8_t lane(uint32_t w, int l) {
+    return (uint8_t)(l ? (w >> 16) : (w & 0xFFFFu));
+  }
+};
+
+template <>
+struct Lanes<uint16_t> {
+  static constexpr int kLanes = 2;
+  __device__ __forceinline__ static uint32_t mn(uint32_t a, uint32_t b) { return __vminu2(a, b); }
+  __device__ __forceinline__ static uint32_t mx(uint32_t a, uint32_t b) { return __vmaxu2(a, b); }
+  __device__ __forceinline__ static uint32_t pack(uint16_t lo, uint16_t hi) {
+    return (uint32_t)lo | ((uint32_t)hi << 16);
+  }
+  __device__ __forceinline__ static uint16_t lane(uint32_t w, int l) {
+    return (uint16_t)(l ? (w >> 16) : (w & 0xFFFFu));
+  }
+};
+
+template <>
+struct Lanes<uint32_t> {
+  static constexpr int kLanes = 1;
+  __device__ __forceinline__ static uint32_t mn(uint32_t a, uint32_t b) { return min(a, b); }
+  __device__ __forceinline__ static uint32_t mx(uint32_t a, uint32_t b) { return max(a, b); }
+  __device__ __forceinline__ static uint32_t pack(uint32_t lo, uint32_t) { return lo; }
+  __device__ __forceinline__ static uint32_t lane(uint32_t w, int) { return w; }
+};
+
+__device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+// Shared-memory row padding: one extra word per 32 so that threads reading
+// with a stride of 2, 4 or 8 words hit distinct banks (x + x/32 swizzle).
+__host__ __device__ constexpr int padded(int x) { return x + (x >> 5); }
+
+// Launch descriptor shared by all kernels: an image (or a band of one) with
+// pitches in elements.  Rows [out_y0, out_y0 + out_h) of the source are
+// filtered into dst rows [0, out_h); reads clamp to source rows [0, src_h)
+// and columns [0, width), which are the *global* image edges -- a band with
+// halo rows simply passes the halo as part of the source.
+//
+// Interleaved planes (H, W, C): `channels` > 1 makes blockIdx.z the channel;
+// element (y, x) of channel c sits at base + y*pitch + x*channels + c.
+struct Job {
+  const void* src;
+  void* dst;
+  int64_t src_pitch;  // elements between rows
+  int64_t dst_pitch;  // elements between rows
+  int width;
+  int src_h;
+  int out_y0;
+  int out_h;
+  int channels;       // x stride in elements; 1 for a plain 2-D image
+};
+
+template <typename T>
+__device__ __forceinline__ T load_px(const Job& job, int y, int x) {
+  const T* s = static_cast<const T*>(job.src) + blockIdx.z;
+  return __ldg(s + (int64_t)y * job.src_pitch + (int64_t)x * job.channels);
+}
+
+template <typename T>
+__device__ __forceinline__ void store_px(const Job& job, int y, int x, T v) {
+  T* d = static_cast<T*>(job.dst) + blockIdx.z;
+  d[(int64_t)y * job.dst_pitch + (int64_t)x * job.channels] = v;
+}
+
+}  // namespace tmb

@@ -1,0 +1,19 @@
+// tm_kernels.h -- internal launcher declarations (not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include "tm_common.cuh"
+
+namespace tmb {
+
+typedef int (*LaunchFn)(const Job&, cudaStream_t);
+
+struct OblEntry {
+  int bits;
+  int k;
+  int tw, th;
+  LaunchFn fn;
+};
+
+int launch_select(int bits, const Job& job, int kw, int kh, cudaStream_t s);
+
+}  // namespace tmb
