@@ -33,6 +33,7 @@ class OblConfig:
     th: int
     bx: int  # tiles per CTA row (per lane)
     by: int  # tile rows per CTA (per lane); == tw for conflict-free loads
+    regs: int = 0  # register budget for program values; 0 = no explicit spilling
 
     @property
     def name(self) -> str:
@@ -50,9 +51,37 @@ OBLIVIOUS_CONFIGS = {
     7: OblConfig(7, 4, 2, 32, 4),
     9: OblConfig(9, 4, 2, 32, 4),
     11: OblConfig(11, 4, 2, 32, 4),
+    13: OblConfig(13, 4, 2, 32, 4),
+    15: OblConfig(15, 4, 4, 32, 4),
+    17: OblConfig(17, 4, 4, 32, 4),
+    19: OblConfig(19, 4, 4, 32, 4),
+    21: OblConfig(21, 4, 4, 32, 4),
 }
 
 DTYPES = {8: "uint8_t", 16: "uint16_t", 32: "uint32_t"}
+
+
+def configs_from_env():
+    """TMB_OBL_CONFIGS="17:4x4:32x4,15:4x4:32x4" overrides the table (experiments)."""
+    spec = os.environ.get("TMB_OBL_CONFIGS")
+    if not spec:
+        return dict(OBLIVIOUS_CONFIGS)
+    out = {}
+    for item in spec.split(","):
+        parts = item.split(":")
+        k, t, b = parts[:3]
+        regs = int(parts[3]) if len(parts) > 3 else 0
+        tw, th = map(int, t.split("x"))
+        bx, by = map(int, b.split("x"))
+        out[int(k)] = OblConfig(int(k), tw, th, bx, by, regs)
+    return out
+
+
+def dtypes_from_env():
+    spec = os.environ.get("TMB_DTYPES")
+    if not spec:
+        return dict(DTYPES)
+    return {int(b): DTYPES[int(b)] for b in spec.split(",")}
 
 
 def emit_colsort(n: int) -> str:
@@ -66,41 +95,156 @@ def emit_colsort(n: int) -> str:
     return "\n".join(lines)
 
 
+def allocate(prog, order, budget: int):
+    """Linear-scan placement of SSA values with an explicit shared-memory spill.
+
+    Walks the emission order keeping at most ``budget`` values in registers.
+    When full it evicts the value whose next use is furthest away (Belady):
+    program inputs (raw pixels, sorted columns) are simply dropped and
+    re-read from their home in shared memory; computed values are stored once
+    into a per-thread spill slot (slot-major, thread-fastest layout: conflict
+    free) and reloaded before their next use.  Returns an event list for the
+    emitter and the number of spill slots.  ``budget <= 0`` disables it.
+    """
+    INF = float("inf")
+    uses: dict[int, list[int]] = {}
+    pos_of = {}
+    for i, v in enumerate(order):
+        pos_of[v] = i
+        _, a, b = prog.values[v]
+        uses.setdefault(a, []).append(i)
+        uses.setdefault(b, []).append(i)
+    outputs = {v for row in prog.outputs for v in row}
+    ptr = {v: 0 for v in uses}
+
+    def next_use(v, i):
+        lst = uses.get(v, ())
+        k = ptr.get(v, 0)
+        while k < len(lst) and lst[k] < i:
+            k += 1
+        ptr[v] = k
+        return lst[k] if k < len(lst) else INF
+
+    regs: set[int] = set()
+    slot_of: dict[int, int] = {}
+    free_slots: list[int] = []
+    n_slots = 0
+    events = []
+
+    def is_input(v):
+        return prog.values[v][0] in ("pix", "col")
+
+    def evict(i, keep):
+        nonlocal n_slots
+        best, best_d = None, -1
+        for r in regs:
+            if r in keep:
+                continue
+            d = next_use(r, i)
+            # dropping an input is cheaper than spilling: prefer it on ties
+            key = (d, 1 if is_input(r) else 0)
+            if best is None or key > best_d:
+                best, best_d = r, key
+        regs.discard(best)
+        if not is_input(best) and best not in slot_of and best_d[0] != INF:
+            if free_slots:
+                sl = free_slots.pop()
+            else:
+                sl = n_slots
+                n_slots += 1
+            slot_of[best] = sl
+            events.append(("spill", best, sl))
+
+    def ensure(v, i, keep):
+        if v in regs:
+            return
+        if budget > 0:
+            while len(regs) >= budget:
+                evict(i, keep)
+        if is_input(v):
+            events.append(("load", v))
+        else:
+            events.append(("reload", v, slot_of[v]))
+        regs.add(v)
+
+    for i, v in enumerate(order):
+        _, a, b = prog.values[v]
+        ensure(a, i, {a, b})
+        ensure(b, i, {a, b})
+        if budget > 0:
+            while len(regs) >= budget:
+                evict(i, {a, b})
+        events.append(("op", v))
+        regs.add(v)
+        for x in (a, b):
+            if next_use(x, i + 1) == INF:
+                regs.discard(x)
+                if x in slot_of:
+                    free_slots.append(slot_of.pop(x))
+        if v in outputs:
+            events.append(("out", v))
+            if next_use(v, i + 1) == INF:
+                regs.discard(v)
+    return events, n_slots
+
+
 def emit_program(cfg: OblConfig) -> tuple[str, dict]:
     prog = build_program(cfg.k, TileDims(cfg.tw, cfg.th))
     order = prog.order()
     name = f"Prog_{cfg.name}"
-    body = []
-    loaded = set()
-    n_mm = 0
-
-    def ref(v: int) -> str:
-        node = prog.values[v]
-        if node[0] in ("pix", "col") and v not in loaded:
-            loaded.add(v)
-            if node[0] == "pix":
-                body.append(f"    const uint32_t v{v} = io.pix({node[1]}, {node[2]});")
-            else:
-                body.append(f"    const uint32_t v{v} = io.col({node[1]}, {node[2]});")
-        return f"v{v}"
-
-    for v in order:
-        kind, a, b = prog.values[v]
-        ra, rb = ref(a), ref(b)
-        fn = "mn" if kind == "min" else "mx"
-        body.append(f"    const uint32_t v{v} = IO::{fn}({ra}, {rb});")
-        n_mm += 1
+    events, n_slots = allocate(prog, order, cfg.regs)
+    where = {}
     for y, row in enumerate(prog.outputs):
         for x, v in enumerate(row):
-            body.append(f"    io.out({x}, {y}, {ref(v)});")
+            where[v] = (x, y)
+    cur: dict[int, str] = {}
+    body = []
+    counter = [0]
+    stats = {"minmax": 0, "loads": 0, "spills": 0, "reloads": 0}
+
+    def fresh(v):
+        counter[0] += 1
+        nm = f"r{counter[0]}"
+        cur[v] = nm
+        return nm
+
+    for ev in events:
+        kind = ev[0]
+        if kind == "load":
+            v = ev[1]
+            node = prog.values[v]
+            fn = "pix" if node[0] == "pix" else "col"
+            body.append(f"    const uint32_t {fresh(v)} = io.{fn}({node[1]}, {node[2]});")
+            stats["loads"] += 1
+        elif kind == "reload":
+            v, sl = ev[1], ev[2]
+            body.append(f"    const uint32_t {fresh(v)} = io.reload({sl});")
+            stats["reloads"] += 1
+        elif kind == "spill":
+            v, sl = ev[1], ev[2]
+            body.append(f"    io.spill({sl}, {cur[v]});")
+            stats["spills"] += 1
+        elif kind == "op":
+            v = ev[1]
+            op, a, b = prog.values[v]
+            fn = "mn" if op == "min" else "mx"
+            ra, rb = cur[a], cur[b]
+            body.append(f"    const uint32_t {fresh(v)} = IO::{fn}({ra}, {rb});")
+            stats["minmax"] += 1
+        else:  # out
+            v = ev[1]
+            x, y = where[v]
+            body.append(f"    io.out({x}, {y}, {cur[v]});")
     head = [f"// generated by paper_2507_19926_b200/codegen.py -- do not edit",
-            f"// kernel {cfg.k}x{cfg.k}, root tile {cfg.tw}x{cfg.th}: {n_mm} min/max per tile,"
-            f" {len(loaded)} shared-memory loads",
+            f"// kernel {cfg.k}x{cfg.k}, root tile {cfg.tw}x{cfg.th}: {stats['minmax']} min/max per"
+            f" tile, {stats['loads']} input loads, {stats['spills']} spills / {stats['reloads']}"
+            f" reloads over {n_slots} slots (register budget {cfg.regs})",
             f"struct {name} {{",
+            f"  static constexpr int kSpillSlots = {n_slots};",
             "  template <class IO>",
             "  __device__ __forceinline__ static void run(IO& io) {"]
-    stats = {"minmax": n_mm, "loads": len(loaded), "peak_live": prog.peak_live(order),
-             "colsort_minmax": prog.colsort_minmax()}
+    stats.update({"peak_live": prog.peak_live(order), "colsort_minmax": prog.colsort_minmax(),
+                  "slots": n_slots})
     return "\n".join(head + body + ["  }", "};", ""]), stats
 
 
@@ -116,7 +260,8 @@ def _write(path: str, text: str) -> None:
 
 def generate(configs=None) -> dict:
     """Write all generated sources; returns per-config stats."""
-    configs = dict(OBLIVIOUS_CONFIGS if configs is None else configs)
+    configs = configs_from_env() if configs is None else dict(configs)
+    dtypes = dtypes_from_env()
     os.makedirs(GEN_DIR, exist_ok=True)
     stats = {}
     col_lens = sorted({c.k - c.th + 1 for c in configs.values()})
@@ -128,27 +273,32 @@ def generate(configs=None) -> dict:
         stats[cfg.k] = st
         _write(os.path.join(GEN_DIR, f"obl_{cfg.name}.cuh"),
                "#pragma once\n#include <cstdint>\nnamespace tmb {\n" + text + "}  // namespace tmb\n")
+    import glob as _glob
+    wanted = set()
     for bits, ctype in DTYPES.items():
-        lines = ["// generated -- oblivious kernel instantiations",
-                 '#include "../tm_oblivious.cuh"', '#include "../tm_launch.cuh"',
-                 '#include "colsort.cuh"']
-        for cfg in configs.values():
-            lines.append(f'#include "obl_{cfg.name}.cuh"')
-        lines.append("namespace tmb {")
+        if bits not in dtypes:
+            continue
         for cfg in configs.values():
             ch = cfg.k - cfg.th + 1
-            lines.append(
-                f"int launch_obl_u{bits}_k{cfg.k}(const Job& job, cudaStream_t s) {{\n"
+            fname = f"obl_inst_u{bits}_{cfg.name}.cu"
+            wanted.add(fname)
+            _write(os.path.join(GEN_DIR, fname), "\n".join([
+                "// generated -- oblivious kernel instantiation",
+                '#include "../tm_oblivious.cuh"', '#include "../tm_launch.cuh"',
+                '#include "colsort.cuh"', f'#include "obl_{cfg.name}.cuh"', "namespace tmb {",
+                f"int launch_obl_u{bits}_k{cfg.k}(const Job& job, cudaStream_t s) {{",
                 f"  return launch_oblivious<{ctype}, {cfg.k}, {cfg.k}, {cfg.tw}, {cfg.th}, "
-                f"{cfg.bx}, {cfg.by}, Prog_{cfg.name}, ColSort{ch}>(job, s);\n}}")
-        lines.append("}  // namespace tmb")
-        _write(os.path.join(GEN_DIR, f"obl_inst_u{bits}.cu"), "\n".join(lines) + "\n")
+                f"{cfg.bx}, {cfg.by}, Prog_{cfg.name}, ColSort{ch}>(job, s);", "}",
+                "}  // namespace tmb", ""]))
+    for stale in _glob.glob(os.path.join(GEN_DIR, "obl_inst_*.cu")):
+        if os.path.basename(stale) not in wanted:
+            os.remove(stale)
     decl = ["// generated -- oblivious launch table (included inside namespace tmb)"]
-    for bits in DTYPES:
+    for bits in dtypes:
         for cfg in configs.values():
             decl.append(f"int launch_obl_u{bits}_k{cfg.k}(const Job&, cudaStream_t);")
     decl.append("static const OblEntry kOblTable[] = {")
-    for bits in DTYPES:
+    for bits in dtypes:
         for cfg in configs.values():
             decl.append(f"  {{{bits}, {cfg.k}, {cfg.tw}, {cfg.th}, &launch_obl_u{bits}_k{cfg.k}}},")
     decl.append("};")

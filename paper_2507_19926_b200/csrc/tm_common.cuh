@@ -90,4 +90,40 @@ __device__ __forceinline__ void store_px(const Job& job, int y, int x, T v) {
   d[(int64_t)y * job.dst_pitch + (int64_t)x * job.channels] = v;
 }
 
+// Store N consecutive pixels of one row starting at x0 (masked at the right
+// edge).  Plain 2-D destinations whose row segment is suitably aligned get one
+// vector store instead of N scalar ones.
+template <typename T, int N>
+__device__ __forceinline__ void store_row(const Job& job, int y, int x0, const T (&v)[N]) {
+  constexpr int kBytes = N * (int)sizeof(T);
+  if (job.channels == 1 && x0 + N <= job.width && (kBytes == 4 || kBytes == 8 || kBytes == 16)) {
+    T* d = static_cast<T*>(job.dst) + (int64_t)y * job.dst_pitch + x0;
+    if ((reinterpret_cast<uintptr_t>(d) & (kBytes - 1)) == 0) {
+      if constexpr (kBytes == 4) {
+        uint32_t w = 0;
+#pragma unroll
+        for (int i = 0; i < N; i++) w |= (uint32_t)v[i] << (8 * sizeof(T) * i);
+        *reinterpret_cast<uint32_t*>(d) = w;
+        return;
+      } else if constexpr (kBytes == 8) {
+        uint64_t w = 0;
+#pragma unroll
+        for (int i = 0; i < N; i++) w |= (uint64_t)v[i] << (8 * sizeof(T) * i);
+        *reinterpret_cast<uint64_t*>(d) = w;
+        return;
+      } else if constexpr (kBytes == 16) {
+        uint32_t w[4] = {0, 0, 0, 0};
+        constexpr int per = 4 / (int)sizeof(T) > 0 ? 4 / (int)sizeof(T) : 1;
+#pragma unroll
+        for (int i = 0; i < N; i++) w[i / per] |= (uint32_t)v[i] << (8 * sizeof(T) * (i % per));
+        *reinterpret_cast<uint4*>(d) = make_uint4(w[0], w[1], w[2], w[3]);
+        return;
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < N; i++)
+    if (x0 + i < job.width) store_px<T>(job, y, x0 + i, v[i]);
+}
+
 }  // namespace tmb
