@@ -44,9 +44,10 @@ int route(int bits, int kw, int kh, int variant) {
     case TM_VARIANT_OBLIVIOUS:
       return obl ? TM_KERNEL_OBLIVIOUS : TM_KERNEL_SELECT;
     case TM_VARIANT_AWARE:
-      return TM_KERNEL_SELECT;
+      return (square && kw >= 9) ? TM_KERNEL_AWARE : TM_KERNEL_SELECT;
     default:  // auto
-      return obl ? TM_KERNEL_OBLIVIOUS : TM_KERNEL_SELECT;
+      if (obl) return TM_KERNEL_OBLIVIOUS;
+      return (square && kw >= 9) ? TM_KERNEL_AWARE : TM_KERNEL_SELECT;
   }
 }
 
@@ -100,6 +101,9 @@ int tm_median2d_band(const void* src, int64_t src_pitch, int32_t src_rows, int32
   switch (route(bits, k_w, k_h, variant)) {
     case TM_KERNEL_OBLIVIOUS:
       err = find_obl(bits, k_w)->fn(job, s);
+      break;
+    case TM_KERNEL_AWARE:
+      err = tmb::launch_aware(bits, job, k_w, s);
       break;
     default:
       err = tmb::launch_select(bits, job, k_w, k_h, s);

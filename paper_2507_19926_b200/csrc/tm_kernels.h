@@ -15,5 +15,6 @@ struct OblEntry {
 };
 
 int launch_select(int bits, const Job& job, int kw, int kh, cudaStream_t s);
+int launch_aware(int bits, const Job& job, int k, cudaStream_t s);
 
 }  // namespace tmb
