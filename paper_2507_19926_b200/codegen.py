@@ -51,7 +51,7 @@ OBLIVIOUS_CONFIGS = {
     7: OblConfig(7, 4, 2, 32, 4),
     9: OblConfig(9, 4, 2, 32, 4),
     11: OblConfig(11, 4, 2, 32, 4),
-    13: OblConfig(13, 4, 2, 32, 4),
+    13: OblConfig(13, 4, 4, 32, 4),
     15: OblConfig(15, 4, 4, 32, 4),
     17: OblConfig(17, 4, 4, 32, 4),
     19: OblConfig(19, 4, 4, 32, 4),
@@ -190,7 +190,7 @@ def allocate(prog, order, budget: int):
 
 def emit_program(cfg: OblConfig) -> tuple[str, dict]:
     prog = build_program(cfg.k, TileDims(cfg.tw, cfg.th))
-    order = prog.order()
+    order = prog.stage_order(eager=True)
     name = f"Prog_{cfg.name}"
     events, n_slots = allocate(prog, order, cfg.regs)
     where = {}

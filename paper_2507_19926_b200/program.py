@@ -48,6 +48,11 @@ class Program:
     _memo: dict = field(default_factory=dict)
     trace: list = field(default_factory=list)    # (label, seen, lo, hi) per candidate merge
     leaf_order: list = field(default_factory=list)  # (x, y) of leaves in split-tree DFS order
+    labels: dict = field(default_factory=dict)      # value id -> (stage kind, node depth)
+    stage_of: dict = field(default_factory=dict)    # value id -> network application index
+    n_stages: int = 0
+    companions: dict = field(default_factory=dict)  # stage -> sibling stages to emit with it
+    _label: tuple = ("input", -1)
 
     cse: bool = True
 
@@ -68,12 +73,18 @@ class Program:
     def col(self, x: int, i: int) -> int:
         return self._mk(("col", x, i))
 
-    def run(self, net, wires: list[int]) -> list[int]:
+    def run(self, net, wires: list[int], label=None) -> list[int]:
         w = list(wires)
+        lab = label or self._label
+        st = self.n_stages
+        self.n_stages += 1
         for i, j in net:
             a, b = w[i], w[j]
             w[i] = self._mk(("min", a, b))
             w[j] = self._mk(("max", a, b))
+            for v in (w[i], w[j]):
+                self.labels.setdefault(v, lab)
+                self.stage_of.setdefault(v, st)
         return w
 
     # ---- analysis -----------------------------------------------------
@@ -141,6 +152,55 @@ class Program:
                         stack.append((node[1], False))
         return out
 
+    def stage_order(self, eager: bool = True) -> list[int]:
+        """Demand-driven over network applications, creation order inside each.
+
+        Post-order DFS over the stage DAG from the leaf medians (split-tree
+        order): a stage (one sorting/merging network) is emitted right before
+        the first stage that needs it, and its comparators in network order,
+        which keeps a merge's live set at its wire count instead of the
+        ~2x that per-output demand order costs.
+        """
+        alive = self.live()
+        ops_of: dict[int, list[int]] = {}
+        preds: dict[int, set] = {}
+        for v, node in enumerate(self.values):
+            if not alive[v] or node[0] not in ("min", "max"):
+                continue
+            st = self.stage_of[v]
+            ops_of.setdefault(st, []).append(v)
+            for a in (node[1], node[2]):
+                sa = self.stage_of.get(a)
+                if sa is not None and sa != st:
+                    preds.setdefault(st, set()).add(sa)
+        done = set()
+        out: list[int] = []
+        leaves = self.leaf_order or [(x, y) for y in range(self.tile.t_h)
+                                     for x in range(self.tile.t_w)]
+        for (lx, ly) in leaves:
+            root = self.stage_of.get(self.outputs[ly][lx])
+            if root is None:
+                continue
+            stack = [(root, False)]
+            while stack:
+                st, expanded = stack.pop()
+                if st in done:
+                    continue
+                if expanded:
+                    done.add(st)
+                    out.extend(ops_of.get(st, ()))
+                    # eager siblings: a split's second candidate merge runs right
+                    # after the first, so the parent window dies before descending
+                    for comp in self.companions.get(st, ()) if eager else ():
+                        if comp not in done:
+                            stack.append((comp, False))
+                else:
+                    stack.append((st, True))
+                    for p in sorted(preds.get(st, ()), reverse=True):
+                        if p not in done:
+                            stack.append((p, False))
+        return out
+
     def peak_live(self, order=None) -> int:
         """Peak simultaneously-live values (inputs count from first use)."""
         order = self.order() if order is None else order
@@ -168,8 +228,17 @@ class Program:
         return peak
 
 
-def build_program(k, tile=None, cse: bool = True) -> Program:
-    """Selection program for kernel ``k`` and root tile ``tile`` (TileDims or side)."""
+def build_program(k, tile=None, cse: bool = True, remat: bool = False,
+                  trim: bool = False) -> Program:
+    """Selection program for kernel ``k`` and root tile ``tile`` (TileDims or side).
+
+    ``remat``: the second child of every split sorts its grown runs straight
+    from the raw pixels (shared-memory inputs) instead of merging its
+    parent's computed runs with the absorbed corners, so no computed run of
+    the parent stays live across the first child's subtree.  Costs a little
+    more min/max (sort(n) instead of merge(n - g, g)), cuts the DFS live
+    state -- the quantity that decides whether a tile fits in 255 registers.
+    """
     kern = as_kernel(k)
     if tile is None:
         tile = min(root_tile_size(max(kern.k_w, kern.k_h)), DRIVER_ROOT_CAP)
@@ -180,17 +249,22 @@ def build_program(k, tile=None, cse: bool = True) -> Program:
     prog = Program(kern, dims, cse=cse)
     n_total = kern.count
 
-    col_runs = {x: [prog.col(x, i) for i in range(root.core_h)]
+    # a run = (sorted SSA values, raw cells it covers, computed?)
+    col_runs = {x: ([prog.col(x, i) for i in range(root.core_h)],
+                    [(x, y) for y in root.core_ys()], False)
                 for x in range(root.fp_x0, root.fp_x0 + root.fp_w)}
     row_sorter = nets.make_sorter(root.core_w)
-    row_runs = {y: prog.run(row_sorter, [prog.pix(x, y) for x in root.core_xs()])
-                for y in root.extra_ys()}
+    row_runs = {}
+    for y in root.extra_ys():
+        cells = [(x, y) for x in root.core_xs()]
+        row_runs[y] = (prog.run(row_sorter, [prog.pix(*c) for c in cells], ("rowsort", 0)),
+                       cells, True)
     corners = {c: prog.pix(*c) for c in root.corners()}
 
     seen = root.core_w * root.core_h
     win = retention_window(n_total, seen)
-    flat = [v for x in root.core_xs() for v in col_runs[x]]
-    merged = prog.run(nets.multiway_merge((root.core_h,) * root.core_w), flat)
+    flat = [v for x in root.core_xs() for v in col_runs[x][0]]
+    merged = prog.run(nets.multiway_merge((root.core_h,) * root.core_w), flat, ("core", 0))
     cand = merged[win.lo - 1: win.hi]
     prog.trace.append(("core", seen, win.lo, win.hi))
     leaves: dict = {}
@@ -201,30 +275,52 @@ def build_program(k, tile=None, cse: bool = True) -> Program:
             leaves[reg.anchor] = cand[0]
             return
         axis, kids = split(reg)
-        for kid in kids:
+        cand_stages = []
+        for ki, kid in enumerate(kids):
+            dep = kid.region.dims.depth
             src = cols if axis == "h" else rows
-            runs = [src[key] for key in kid.gained]
+            runs = [src[key][0] for key in kid.gained]
             if len(runs) == 1:
                 pack = runs[0]
             else:
                 sizes = tuple(len(r) for r in runs)
-                pack = prog.run(nets.multiway_merge(sizes), [v for r in runs for v in r])
+                pack = prog.run(nets.multiway_merge(sizes), [v for r in runs for v in r],
+                                ("pack", dep))
             seen2 = seen + len(pack)
             w = retention_window(n_total, seen2)
             lo, hi = w.lo - 1 - d_lo, w.hi - 1 - d_lo
             assert 0 <= lo <= hi < len(cand) + len(pack)
-            both = prog.run(nets.oddeven_merge(len(cand), len(pack)), list(cand) + list(pack))
+            ca, pa = list(cand), list(pack)
+            if trim:
+                # drop inputs that provably sit above / below the kept window:
+                # x[i] lands at merged position i .. i + len(other)
+                lo_a = max(0, lo - len(pa))          # cand[i], i < lo_a: always below
+                lo_b = max(0, lo - len(ca))
+                ca = ca[lo_a: hi + 1]
+                pa = pa[lo_b: hi + 1]
+                lo, hi = lo - lo_a - lo_b, hi - lo_a - lo_b
+            both = prog.run(nets.oddeven_merge(len(ca), len(pa)), ca + pa, ("cand", dep))
+            cand_stages.append(prog.n_stages - 1)
+            if len(cand_stages) == 2:
+                prog.companions[cand_stages[0]] = [cand_stages[1]]
             kid_cand = both[lo: hi + 1]
             prog.trace.append((f"cand {kid.region.dims.t_w}x{kid.region.dims.t_h}",
                                seen2, w.lo, w.hi))
             other = rows if axis == "h" else cols
             grown = {}
             for key, cells in kid.grown:
-                add = [corn[c] for c in cells]
-                if len(add) > 1:
-                    add = prog.run(nets.make_sorter(len(add)), add)
-                base = other[key]
-                grown[key] = prog.run(nets.oddeven_merge(len(base), len(add)), base + add)
+                base, bcells, computed = other[key]
+                allcells = list(bcells) + list(cells)
+                if remat and ki == 1 and computed:
+                    vals = prog.run(nets.make_sorter(len(allcells)),
+                                    [prog.pix(*c) for c in allcells], ("rowsort", dep))
+                else:
+                    add = [corn[c] for c in cells]
+                    if len(add) > 1:
+                        add = prog.run(nets.make_sorter(len(add)), add, ("cornersort", dep))
+                    vals = prog.run(nets.oddeven_merge(len(base), len(add)), base + add,
+                                    ("extend", dep))
+                grown[key] = (vals, allcells, True)
             if axis == "h":
                 kcols = {x: cols[x] for x in kid.region.extra_xs()}
                 krows = grown
