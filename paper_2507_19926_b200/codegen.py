@@ -34,10 +34,11 @@ class OblConfig:
     bx: int  # tiles per CTA row (per lane)
     by: int  # tile rows per CTA (per lane); == tw for conflict-free loads
     regs: int = 0  # register budget for program values; 0 = no explicit spilling
+    pair: bool = False  # split each root tile over a thread pair (pairgen.py)
 
     @property
     def name(self) -> str:
-        return f"k{self.k}_t{self.tw}x{self.th}"
+        return f"k{self.k}_t{self.tw}x{self.th}" + ("p" if self.pair else "")
 
     @property
     def threads(self) -> int:
@@ -53,9 +54,14 @@ OBLIVIOUS_CONFIGS = {
     11: OblConfig(11, 4, 2, 32, 4),
     13: OblConfig(13, 4, 4, 32, 4),
     15: OblConfig(15, 4, 4, 32, 4),
-    17: OblConfig(17, 4, 4, 32, 4),
-    19: OblConfig(19, 4, 4, 32, 4),
-    21: OblConfig(21, 4, 4, 32, 4),
+    # k >= 17: a 4x4 root tile's live state exceeds the register file of one
+    # thread -- split each tile over a thread pair (pairgen.py)
+    17: OblConfig(17, 4, 4, 32, 4, pair=True),
+    19: OblConfig(19, 4, 4, 32, 4, pair=True),
+    21: OblConfig(21, 4, 4, 32, 4, pair=True),
+    23: OblConfig(23, 4, 4, 32, 4, pair=True),
+    25: OblConfig(25, 4, 4, 32, 4, pair=True),
+    27: OblConfig(27, 4, 4, 32, 4, pair=True),
 }
 
 DTYPES = {8: "uint8_t", 16: "uint16_t", 32: "uint32_t"}
@@ -70,10 +76,11 @@ def configs_from_env():
     for item in spec.split(","):
         parts = item.split(":")
         k, t, b = parts[:3]
-        regs = int(parts[3]) if len(parts) > 3 else 0
+        regs = int(parts[3]) if len(parts) > 3 and parts[3] != "p" else 0
+        pair = "p" in parts[3:]
         tw, th = map(int, t.split("x"))
         bx, by = map(int, b.split("x"))
-        out[int(k)] = OblConfig(int(k), tw, th, bx, by, regs)
+        out[int(k)] = OblConfig(int(k), tw, th, bx, by, regs, pair)
     return out
 
 
@@ -241,6 +248,9 @@ def emit_program(cfg: OblConfig) -> tuple[str, dict]:
             f" reloads over {n_slots} slots (register budget {cfg.regs})",
             f"struct {name} {{",
             f"  static constexpr int kSpillSlots = {n_slots};",
+            "  static constexpr int kPair = 0;",
+            "  static constexpr int kCoreHalf = 0;",
+            "  static constexpr int kRowShift = 0;",
             "  template <class IO>",
             "  __device__ __forceinline__ static void run(IO& io) {"]
     stats.update({"peak_live": prog.peak_live(order), "colsort_minmax": prog.colsort_minmax(),
@@ -269,7 +279,11 @@ def generate(configs=None) -> dict:
            "// generated -- column sorting networks\n#pragma once\n#include <cstdint>\n"
            "namespace tmb {\n" + "".join(emit_colsort(n) for n in col_lens) + "}  // namespace tmb\n")
     for cfg in configs.values():
-        text, st = emit_program(cfg)
+        if cfg.pair:
+            from .pairgen import emit_pair_program
+            text, st = emit_pair_program(cfg.k, cfg.tw, cfg.th, f"Prog_{cfg.name}")
+        else:
+            text, st = emit_program(cfg)
         stats[cfg.k] = st
         _write(os.path.join(GEN_DIR, f"obl_{cfg.name}.cuh"),
                "#pragma once\n#include <cstdint>\nnamespace tmb {\n" + text + "}  // namespace tmb\n")

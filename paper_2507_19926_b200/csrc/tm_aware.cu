@@ -597,6 +597,16 @@ static int launch_t(const Job& job0, int k, cudaStream_t s, long budget) {
 
 int launch_aware(int bits, const Job& job, int k, cudaStream_t s) {
   const long budget = 3L << 30;  // device bytes per band
+  // keep freed pass buffers in the stream-ordered pool between calls
+  // (the default release threshold of 0 returns them to the OS at every sync)
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
   switch (bits) {
     case 8: return aware::launch_t<uint8_t>(job, k, s, budget);
     case 16: return aware::launch_t<uint16_t>(job, k, s, budget);

@@ -15,7 +15,7 @@ inline cudaError_t ensure_smem(F fn, int bytes) {
 
 template <typename T, int KW, int KH, int TW, int TH, int BX, int BY, class Prog, class CSort>
 int launch_oblivious(const Job& job, cudaStream_t stream) {
-  using Lay = OblLayout<T, KW, KH, TW, TH, BX, BY, Prog::kSpillSlots>;
+  using Lay = OblLayout<T, KW, KH, TW, TH, BX, BY, Prog::kSpillSlots, Prog::kPair>;
   auto fn = obl_kernel<T, KW, KH, TW, TH, BX, BY, Prog, CSort>;
   cudaError_t e = ensure_smem(fn, Lay::kSmemBytes);
   if (e != cudaSuccess) return (int)e;

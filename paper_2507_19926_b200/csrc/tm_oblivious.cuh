@@ -43,11 +43,11 @@ __host__ __device__ constexpr int stride_1mod32(int words) {
   return words + ((33 - (words & 31)) & 31);
 }
 
-template <typename T, int KW, int KH, int TW, int TH, int BX, int BY, int S>
+template <typename T, int KW, int KH, int TW, int TH, int BX, int BY, int S, int PAIR = 0>
 struct OblLayout {
   using G = OblGeom<T, KW, KH, TW, TH>;
   static constexpr int kLanes = Lanes<T>::kLanes;
-  static constexpr int kThreads = BX * BY;
+  static constexpr int kThreads = BX * BY * (PAIR ? 2 : 1);
   static constexpr int OW = BX * TW;             // output columns per CTA
   static constexpr int OH = BY * TH;             // output rows per lane per CTA
   static constexpr int FW = OW + KW - 1;         // footprint columns per CTA
@@ -85,10 +85,44 @@ struct OblIO {
   __device__ __forceinline__ void out(int x, int y, uint32_t v) const { outp[y * Lay::OW + x] = v; }
 };
 
+// Pair I/O (pairgen.py): thread `role` of a lane pair works on one root tile;
+// *_t accessors translate the root-phase halves, *_m mirror the child phase
+// (x -> TW-1-x for role 1), xchg swaps a value with the partner lane.
+template <typename T, class Lay, class Prog>
+struct PairIO {
+  using G = typename Lay::G;
+  const uint32_t* raw_t;   // root phase rows: footprint row 0 + role * kRowShift
+  const uint32_t* col_tb;  // root phase core halves: + role * kCoreHalf columns
+  const uint32_t* raw_m;   // child phase: mirrored column origin
+  const uint32_t* col_mb;
+  uint32_t* out_mb;
+  int s;                   // +1 (role 0) or -1 (role 1)
+  int role;
+  __device__ __forceinline__ uint32_t pix_t(int x, int y) const {
+    return raw_t[(y + G::HH) * Lay::P + (x + G::HW)];
+  }
+  __device__ __forceinline__ uint32_t col_t(int x, int i) const {
+    return col_tb[i * Lay::P + (x + G::HW)];
+  }
+  __device__ __forceinline__ uint32_t pix_m(int x, int y) const {
+    return raw_m[(y + G::HH) * Lay::P + s * x];
+  }
+  __device__ __forceinline__ uint32_t col_m(int x, int i) const {
+    return col_mb[i * Lay::P + s * x];
+  }
+  __device__ __forceinline__ void out_m(int x, int y, uint32_t v) const {
+    out_mb[y * Lay::OW + s * x] = v;
+  }
+  __device__ __forceinline__ static uint32_t xchg(uint32_t v) { return __shfl_xor_sync(0xffffffffu, v, 1); }
+  __device__ __forceinline__ uint32_t sel(uint32_t a, uint32_t b) const { return role ? b : a; }
+  __device__ __forceinline__ static uint32_t mn(uint32_t a, uint32_t b) { return Lanes<T>::mn(a, b); }
+  __device__ __forceinline__ static uint32_t mx(uint32_t a, uint32_t b) { return Lanes<T>::mx(a, b); }
+};
+
 template <typename T, int KW, int KH, int TW, int TH, int BX, int BY, class Prog, class CSort>
-__global__ void __launch_bounds__(BX * BY)
+__global__ void __launch_bounds__(BX * BY * (Prog::kPair ? 2 : 1))
 obl_kernel(Job job) {
-  using Lay = OblLayout<T, KW, KH, TW, TH, BX, BY, Prog::kSpillSlots>;
+  using Lay = OblLayout<T, KW, KH, TW, TH, BX, BY, Prog::kSpillSlots, Prog::kPair>;
   using G = OblGeom<T, KW, KH, TW, TH>;
   using L = Lanes<T>;
   constexpr int NT = Lay::kThreads;
@@ -137,7 +171,22 @@ obl_kernel(Job job) {
   __syncthreads();
 
   // ---- stage 3: per-thread selection program -----------------------------
-  {
+  if constexpr (Prog::kPair) {
+    const int role = tid & 1, pr = tid >> 1;
+    const int by = pr % BY;
+    const int bx = pr / BY;
+    const uint32_t* rt = raw + by * TH * Lay::P + bx * TW;
+    const uint32_t* st = scol + by * Lay::SB + bx * TW;
+    PairIO<T, Lay, Prog> io;
+    io.role = role;
+    io.s = 1 - 2 * role;
+    io.raw_t = rt + role * Prog::kRowShift * Lay::P;
+    io.col_tb = st + role * Prog::kCoreHalf;
+    io.raw_m = rt + G::HW + role * (TW - 1);
+    io.col_mb = st + G::HW + role * (TW - 1);
+    io.out_mb = outt + by * TH * Lay::OW + bx * TW + role * (TW - 1);
+    Prog::run(io);
+  } else {
     const int by = tid % BY;
     const int bx = tid / BY;
     OblIO<T, Lay> io;

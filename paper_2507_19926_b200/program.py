@@ -52,6 +52,8 @@ class Program:
     stage_of: dict = field(default_factory=dict)    # value id -> network application index
     n_stages: int = 0
     companions: dict = field(default_factory=dict)  # stage -> sibling stages to emit with it
+    root_cand: list = field(default_factory=list)   # value ids of the root candidate window
+    root_rows: dict = field(default_factory=dict)   # y -> value ids of the root's sorted extra rows
     _label: tuple = ("input", -1)
 
     cse: bool = True
@@ -266,6 +268,8 @@ def build_program(k, tile=None, cse: bool = True, remat: bool = False,
     flat = [v for x in root.core_xs() for v in col_runs[x][0]]
     merged = prog.run(nets.multiway_merge((root.core_h,) * root.core_w), flat, ("core", 0))
     cand = merged[win.lo - 1: win.hi]
+    prog.root_cand = list(cand)
+    prog.root_rows = {y: list(r[0]) for y, r in row_runs.items()}
     prog.trace.append(("core", seen, win.lo, win.hi))
     leaves: dict = {}
 
