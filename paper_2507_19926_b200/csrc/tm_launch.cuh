@@ -25,8 +25,8 @@ int launch_oblivious(const Job& job, cudaStream_t stream) {
   }();
   if (carve >= 0) cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
   const int rows_per_cta = Lay::OH * Lay::kLanes;
-  dim3 grid((job.width + Lay::OW - 1) / Lay::OW, (job.out_h + rows_per_cta - 1) / rows_per_cta,
-            job.channels);
+  dim3 grid(((job.width + Lay::OW - 1) / Lay::OW) * job.channels,
+            (job.out_h + rows_per_cta - 1) / rows_per_cta, 1);
   fn<<<grid, Lay::kThreads, Lay::kSmemBytes, stream>>>(job);
   return (int)cudaGetLastError();
 }

@@ -121,8 +121,16 @@ struct PairIO {
 
 template <typename T, int KW, int KH, int TW, int TH, int BX, int BY, class Prog, class CSort>
 __global__ void __launch_bounds__(BX * BY * (Prog::kPair ? 2 : 1))
-obl_kernel(Job job) {
+obl_kernel(Job job0) {
   using Lay = OblLayout<T, KW, KH, TW, TH, BX, BY, Prog::kSpillSlots, Prog::kPair>;
+  // channels are interleaved into blockIdx.x (c fastest) so the CTAs of all
+  // planes of one image region run together and share L2 sectors of the
+  // interleaved (H, W, C) buffer -- both for the loads and the byte stores
+  Job job = job0;
+  const int chan = blockIdx.x % job0.channels;
+  const int tile_x = blockIdx.x / job0.channels;
+  job.src = static_cast<const T*>(job0.src) + chan;
+  job.dst = static_cast<T*>(job0.dst) + chan;
   using G = OblGeom<T, KW, KH, TW, TH>;
   using L = Lanes<T>;
   constexpr int NT = Lay::kThreads;
@@ -134,7 +142,7 @@ obl_kernel(Job job) {
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  const int X0 = blockIdx.x * Lay::OW;
+  const int X0 = tile_x * Lay::OW;
   const int Y0 = blockIdx.y * Lay::OH * Lay::kLanes;  // output row (band-relative) of lane 0
   const int W = job.width, SH = job.src_h;
   const int sy0 = job.out_y0 + Y0 - G::HH;             // source row of footprint row 0, lane 0
