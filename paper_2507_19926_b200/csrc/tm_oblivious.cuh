@@ -141,23 +141,34 @@ obl_kernel(Job job0) {
   uint32_t* outt = spill + Lay::kSpillWords;
 
   const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
   const int X0 = tile_x * Lay::OW;
   const int Y0 = blockIdx.y * Lay::OH * Lay::kLanes;  // output row (band-relative) of lane 0
   const int W = job.width, SH = job.src_h;
   const int sy0 = job.out_y0 + Y0 - G::HH;             // source row of footprint row 0, lane 0
 
   // ---- stage 1: footprint -> shared memory lane words ---------------------
-  // warp-per-row, lane-per-column; each source element is read once.
-  for (int r = warp; r < Lay::RH; r += NT / 32) {
-    const int ya = clampi(sy0 + r, 0, SH - 1);
-    const int yb = clampi(sy0 + Lay::OH + r, 0, SH - 1);
-    uint32_t* row = raw + r * Lay::P;
-    for (int c = lane; c < Lay::FW; c += 32) {
-      const int gx = clampi(X0 + c - G::HW, 0, W - 1);
-      const T a = load_px<T>(job, ya, gx);
-      const T b = Lay::kLanes == 2 ? load_px<T>(job, yb, gx) : a;
-      row[c] = L::pack(a, b);
+  // Every thread issues all of its global loads before consuming any (the
+  // CTA's footprint is loaded with E loads in flight per thread instead of
+  // one round trip per element), then packs and stores them.
+  {
+    constexpr int kItems = Lay::RH * Lay::FW;
+    constexpr int E = (kItems + NT - 1) / NT;
+    T va[E], vb[E];
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+      const int idx = tid + e * NT;
+      const int r = idx / Lay::FW, c = idx - (idx / Lay::FW) * Lay::FW;
+      if (idx < kItems) {
+        const int gx = clampi(X0 + c - G::HW, 0, W - 1);
+        va[e] = load_px<T>(job, clampi(sy0 + r, 0, SH - 1), gx);
+        vb[e] = Lay::kLanes == 2 ? load_px<T>(job, clampi(sy0 + Lay::OH + r, 0, SH - 1), gx) : va[e];
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+      const int idx = tid + e * NT;
+      const int r = idx / Lay::FW, c = idx - (idx / Lay::FW) * Lay::FW;
+      if (idx < kItems) raw[r * Lay::P + c] = L::pack(va[e], vb[e]);
     }
   }
   __syncthreads();
