@@ -48,7 +48,8 @@ enum {
   TM_KERNEL_NONE = 0,
   TM_KERNEL_OBLIVIOUS = 1, /* register-resident selection network, variant (1) */
   TM_KERNEL_AWARE = 2,     /* shared-memory rank selection, variant (2) */
-  TM_KERNEL_SELECT = 3     /* brute-force per-pixel radix selection ("oracle") */
+  TM_KERNEL_SELECT = 3,    /* brute-force per-pixel radix selection ("oracle") */
+  TM_KERNEL_HISTOGRAM = 4  /* 8-bit sliding column histograms, variant (2) */
 };
 
 enum { TM_OK = 0, TM_EINVAL = 1, TM_ETYPE = 2, TM_ECUDA = 3 };
@@ -87,6 +88,11 @@ int tm_median2d_host(const void* src, int64_t src_pitch, void* dst, int64_t dst_
 /* Which kernel serves (bits, k_w, k_h, variant); TM_KERNEL_NONE if invalid. */
 int tm_dispatch_query(int32_t bits, int32_t k_w, int32_t k_h, int32_t variant);
 const char* tm_kernel_name(int32_t kernel);
+
+/* Diagnostics (sweeps, tests): force the calling thread's launches onto one
+ * kernel when it supports (bits, k); 0 restores the dispatch table.  Returns
+ * the previous setting.  Results do not change -- every kernel is exact. */
+int tm_force_kernel(int32_t kernel);
 
 /* Number of kernel launches issued by this process so far (all entry points). */
 int64_t tm_launch_count(void);

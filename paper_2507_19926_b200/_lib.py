@@ -14,7 +14,8 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libtilemedian_b200.so")
 
 VARIANT_CODES = {"auto": 0, "oblivious": 1, "aware": 2, "oracle": 3}
-KERNEL_NAMES = {0: "none", 1: "oblivious", 2: "aware", 3: "select"}
+KERNEL_NAMES = {0: "none", 1: "oblivious", 2: "aware", 3: "select", 4: "histogram"}
+KERNEL_CODES = {v: k for k, v in KERNEL_NAMES.items()}
 TM_OK, TM_EINVAL, TM_ETYPE, TM_ECUDA = 0, 1, 2, 3
 
 _lock = threading.Lock()
@@ -34,6 +35,7 @@ _SIGS = {
                                         c_i32, c_i32, c_i32]),
     "tm_dispatch_query": (ctypes.c_int, [c_i32, c_i32, c_i32, c_i32]),
     "tm_kernel_name": (ctypes.c_char_p, [c_i32]),
+    "tm_force_kernel": (ctypes.c_int, [c_i32]),
     "tm_launch_count": (ctypes.c_int64, []),
     "tm_last_error": (ctypes.c_char_p, []),
     "tm_version": (ctypes.c_char_p, []),

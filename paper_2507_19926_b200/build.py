@@ -25,7 +25,8 @@ LIB = os.path.join(PKG, "libtilemedian_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
-         "--expt-relaxed-constexpr"]
+         "--expt-relaxed-constexpr", "-diag-suppress", "177",
+         *os.environ.get("TMB_NVCC_EXTRA", "").split()]
 
 
 def _sources() -> list[str]:

@@ -17,6 +17,7 @@ namespace tmb {
 namespace {
 
 thread_local char g_err[512] = "";
+thread_local int g_force = 0;
 std::atomic<int64_t> g_launches{0};
 
 int fail(int code, const char* fmt, ...) {
@@ -35,7 +36,26 @@ const tmb::OblEntry* find_obl(int bits, int k) {
 
 // Kernel routing.  Results are identical whichever exact kernel runs; the
 // variant only chooses the algorithm (engine.py:36-52).
+bool supports(int kernel, int bits, int kw, int kh) {
+  const bool square = kw == kh;
+  switch (kernel) {
+    case TM_KERNEL_OBLIVIOUS: return square && find_obl(bits, kw) != nullptr;
+    case TM_KERNEL_AWARE: return square && kw >= 9;
+    case TM_KERNEL_SELECT: return true;
+    case TM_KERNEL_HISTOGRAM: return square && bits == 8 && tmb::hist8_supports(kw);
+    default: return false;
+  }
+}
+
+// The fastest exact kernel for (bits, k) on B200, from measured sweeps
+// (profiles/).
+int best_aware(int bits, int k) {
+  if (bits == 8 && tmb::hist8_supports(k)) return TM_KERNEL_HISTOGRAM;
+  return TM_KERNEL_AWARE;
+}
+
 int route(int bits, int kw, int kh, int variant) {
+  if (g_force && supports(g_force, bits, kw, kh)) return g_force;
   const bool square = kw == kh;
   const bool obl = square && find_obl(bits, kw) != nullptr;
   switch (variant) {
@@ -44,10 +64,10 @@ int route(int bits, int kw, int kh, int variant) {
     case TM_VARIANT_OBLIVIOUS:
       return obl ? TM_KERNEL_OBLIVIOUS : TM_KERNEL_SELECT;
     case TM_VARIANT_AWARE:
-      return (square && kw >= 9) ? TM_KERNEL_AWARE : TM_KERNEL_SELECT;
+      return (square && kw >= 9) ? best_aware(bits, kw) : TM_KERNEL_SELECT;
     default:  // auto
       if (obl) return TM_KERNEL_OBLIVIOUS;
-      return (square && kw >= 9) ? TM_KERNEL_AWARE : TM_KERNEL_SELECT;
+      return (square && kw >= 9) ? best_aware(bits, kw) : TM_KERNEL_SELECT;
   }
 }
 
@@ -104,6 +124,9 @@ int tm_median2d_band(const void* src, int64_t src_pitch, int32_t src_rows, int32
       break;
     case TM_KERNEL_AWARE:
       err = tmb::launch_aware(bits, job, k_w, s);
+      break;
+    case TM_KERNEL_HISTOGRAM:
+      err = tmb::launch_hist8(job, k_w, s);
       break;
     default:
       err = tmb::launch_select(bits, job, k_w, k_h, s);
@@ -192,8 +215,15 @@ const char* tm_kernel_name(int32_t kernel) {
     case TM_KERNEL_OBLIVIOUS: return "oblivious";
     case TM_KERNEL_AWARE: return "aware";
     case TM_KERNEL_SELECT: return "select";
+    case TM_KERNEL_HISTOGRAM: return "histogram";
     default: return "none";
   }
+}
+
+int tm_force_kernel(int32_t kernel) {
+  const int prev = g_force;
+  g_force = kernel;
+  return prev;
 }
 
 int64_t tm_launch_count(void) { return g_launches.load(); }

@@ -29,6 +29,9 @@ def main():
     ap.add_argument("--bits", type=int, nargs="+", default=[8, 16, 32])
     ap.add_argument("--k", type=int, nargs="+", default=[3, 5, 7, 9, 11])
     ap.add_argument("--variants", nargs="+", default=["auto"])
+    ap.add_argument("--kernels", nargs="+", default=None,
+                    help="force kernels by name (oblivious, aware, select, histogram, ...) "
+                         "instead of iterating variants")
     ap.add_argument("--reps", type=int, default=20)
     a = ap.parse_args()
     lib = _lib.load()
@@ -41,9 +44,14 @@ def main():
         esz = bits // 8
         for k in a.k:
             W = op_model(k)["minmax_per_pixel"]
-            for v in a.variants:
-                code = _lib.VARIANT_CODES[v]
+            runs = ([("forced:" + kn, kn) for kn in a.kernels] if a.kernels
+                    else [(v, None) for v in a.variants])
+            for v, forced in runs:
+                code = _lib.VARIANT_CODES["auto" if forced else v]
+                lib.tm_force_kernel(_lib.KERNEL_CODES[forced] if forced else 0)
                 kern = lib.tm_kernel_name(lib.tm_dispatch_query(bits, k, k, code)).decode()
+                if forced and kern != forced:
+                    continue
                 s = torch.cuda.current_stream().cuda_stream
                 def run():
                     _lib.check(lib.tm_median2d(src.data_ptr(), n * esz, dst.data_ptr(), n * esz,
