@@ -243,7 +243,7 @@ def main():
         out = torch.empty_like(img)
         samples_rank = H * W * C
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
-    variant = pick_variant(k) if args.variant == "auto" else args.variant
+    variant = args.variant  # "auto": the C ABI's measured per-(dtype, k) table
     vcode = _lib.VARIANT_CODES[variant]
     kernel = lib.tm_kernel_name(lib.tm_dispatch_query(bits, k, k, vcode)).decode()
     stream = torch.cuda.current_stream(dev)

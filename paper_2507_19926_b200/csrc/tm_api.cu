@@ -57,12 +57,15 @@ int best_aware(int bits, int k) {
 int route(int bits, int kw, int kh, int variant) {
   if (g_force && supports(g_force, bits, kw, kh)) return g_force;
   const bool square = kw == kh;
-  const bool obl = square && find_obl(bits, kw) != nullptr;
+  // 8-bit data: the sliding-histogram kernel overtakes the oblivious network
+  // from k = 15 on (profiles/r01_sweep_4096_hist.jsonl).
+  const bool obl = square && find_obl(bits, kw) != nullptr &&
+                   !(bits == 8 && kw >= 15 && tmb::hist8_supports(kw));
   switch (variant) {
     case TM_VARIANT_ORACLE:
       return TM_KERNEL_SELECT;
     case TM_VARIANT_OBLIVIOUS:
-      return obl ? TM_KERNEL_OBLIVIOUS : TM_KERNEL_SELECT;
+      return (square && find_obl(bits, kw)) ? TM_KERNEL_OBLIVIOUS : TM_KERNEL_SELECT;
     case TM_VARIANT_AWARE:
       return (square && kw >= 9) ? best_aware(bits, kw) : TM_KERNEL_SELECT;
     default:  // auto

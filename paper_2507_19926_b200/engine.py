@@ -143,6 +143,10 @@ def filter_image(image, k, variant="auto", *, root=None, workers=1, slice_budget
     """
     if variant not in VARIANTS:
         raise ValueError(f"unknown variant {variant!r} (expected one of {VARIANTS})")
+    # the reference resolves "auto" to an engine name (validation and
+    # instrumentation follow it); the C ABI gets "auto" so its measured
+    # per-(dtype, k) table picks the fastest exact kernel
+    launch = variant
     if variant == "auto":
         variant = pick_variant(k)
     torch_in = _is_torch(image)
@@ -172,8 +176,8 @@ def filter_image(image, k, variant="auto", *, root=None, workers=1, slice_budget
             raise ValueError("expected a 2-D image")
         if 0 in shape:
             raise ValueError(f"image dims must be positive, got {shape[1]}x{shape[0]}")
-    out = (_run_torch(img, kern.k_w, kern.k_h, variant) if torch_in
-           else _run_numpy(img, kern.k_w, kern.k_h, variant, device))
+    out = (_run_torch(img, kern.k_w, kern.k_h, launch) if torch_in
+           else _run_numpy(img, kern.k_w, kern.k_h, launch, device))
     if variant == "aware" and (counter is not None or checksums is not None):
         H, W = shape
         itemsize = img.element_size() if torch_in else img.itemsize
@@ -219,8 +223,8 @@ def filter_planes(image, k, variant="auto", **kwargs):
     probe = np.empty((1, 1), dtype=np.uint8)
     _validate_like_plane(probe, k, v, kwargs.get("root"))
     kern = as_kernel(k)
-    return (_run_torch(img, kern.k_w, kern.k_h, v) if torch_in
-            else _run_numpy(img, kern.k_w, kern.k_h, v, int(kwargs.get("device", 0))))
+    return (_run_torch(img, kern.k_w, kern.k_h, variant) if torch_in
+            else _run_numpy(img, kern.k_w, kern.k_h, variant, int(kwargs.get("device", 0))))
 
 
 def _validate_like_plane(probe, k, variant, root) -> None:
@@ -241,8 +245,6 @@ def _validate_like_plane(probe, k, variant, root) -> None:
 def dispatch_query(dtype, k, variant="auto") -> str:
     """Name of the kernel the C ABI runs for (dtype, k, variant)."""
     kern = as_kernel(k)
-    if variant == "auto":
-        variant = pick_variant(k)
     code = _lib.load().tm_dispatch_query(_bits_of(dtype), kern.k_w, kern.k_h,
                                          _lib.VARIANT_CODES[variant])
     return _lib.KERNEL_NAMES.get(code, "none")

@@ -1,3 +1,2 @@
-ncu --set full --clock-control none --import-source on -k regex:hist8 -s 1 -c 1 -o gpurun_out/hist17 python tools/one.py --bits 8 --k 17 --kernel histogram --reps 2 > gpurun_out/prof_hist.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:hist8 -s 1 -c 1 -o gpurun_out/hist3 python tools/one.py --bits 8 --k 3 --kernel histogram --reps 2 >> gpurun_out/prof_hist.log 2>&1
-tail -5 gpurun_out/prof_hist.log
+ncu --set full --clock-control none --import-source on -k regex:hist8 -s 1 -c 1 -o gpurun_out/h3_17 python tools/one.py --bits 8 --k 17 --kernel histogram --reps 2 > gpurun_out/prof_hist.log 2>&1
+tail -2 gpurun_out/prof_hist.log
