@@ -49,7 +49,8 @@ enum {
   TM_KERNEL_OBLIVIOUS = 1, /* register-resident selection network, variant (1) */
   TM_KERNEL_AWARE = 2,     /* shared-memory rank selection, variant (2) */
   TM_KERNEL_SELECT = 3,    /* brute-force per-pixel radix selection ("oracle") */
-  TM_KERNEL_HISTOGRAM = 4  /* 8-bit sliding column histograms, variant (2) */
+  TM_KERNEL_HISTOGRAM = 4, /* 8-bit sliding column histograms, variant (2) */
+  TM_KERNEL_RANK = 5       /* 16/32-bit: coarse + candidate-key histogram sweeps, variant (2) */
 };
 
 enum { TM_OK = 0, TM_EINVAL = 1, TM_ETYPE = 2, TM_ECUDA = 3 };

@@ -43,6 +43,7 @@ bool supports(int kernel, int bits, int kw, int kh) {
     case TM_KERNEL_AWARE: return square && kw >= 9;
     case TM_KERNEL_SELECT: return true;
     case TM_KERNEL_HISTOGRAM: return square && bits == 8 && tmb::hist8_supports(kw);
+    case TM_KERNEL_RANK: return square && tmb::rank_supports(bits, kw);
     default: return false;
   }
 }
@@ -51,6 +52,7 @@ bool supports(int kernel, int bits, int kw, int kh) {
 // (profiles/).
 int best_aware(int bits, int k) {
   if (bits == 8 && tmb::hist8_supports(k)) return TM_KERNEL_HISTOGRAM;
+  if (tmb::rank_supports(bits, k)) return TM_KERNEL_RANK;
   return TM_KERNEL_AWARE;
 }
 
@@ -130,6 +132,9 @@ int tm_median2d_band(const void* src, int64_t src_pitch, int32_t src_rows, int32
       break;
     case TM_KERNEL_HISTOGRAM:
       err = tmb::launch_hist8(job, k_w, s);
+      break;
+    case TM_KERNEL_RANK:
+      err = tmb::launch_rank(bits, job, k_w, s);
       break;
     default:
       err = tmb::launch_select(bits, job, k_w, k_h, s);
@@ -219,6 +224,7 @@ const char* tm_kernel_name(int32_t kernel) {
     case TM_KERNEL_AWARE: return "aware";
     case TM_KERNEL_SELECT: return "select";
     case TM_KERNEL_HISTOGRAM: return "histogram";
+    case TM_KERNEL_RANK: return "rank";
     default: return "none";
   }
 }

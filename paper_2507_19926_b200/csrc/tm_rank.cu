@@ -1,0 +1,415 @@
+// tm_rank.cu -- data-aware O(k) median for 16- and 32-bit images (variant (2)
+// for uint16 / uint32): the sliding-histogram sweep (tm_sweep.cuh) run twice
+// on 6-bit KEYS derived from the samples.
+//
+// Reference role: the data-aware engine (aware.py:437-492) -- the candidates
+// for a tile of outputs are narrowed with a cheap pass, then the median is
+// selected exactly by rank among the survivors (the paper's forgetful
+// candidate windows, section 5.1, applied per tile of outputs).
+//
+// One warp = one work item: 64 output columns x up to RMAX output rows.
+//  1. coarse pass: sweep with key = the top 6 bits of each sample.  Gives every
+//     output pixel the exact 6-bit prefix of its median; every median of the
+//     item lies in [lo, hi] = [B_lo << s, ((B_hi + 1) << s) - 1].
+//  2. fine keys: 0 below lo, 63 above hi, 1 + ((v - lo) >> f) inside, with the
+//     smallest f that maps [lo, hi] onto at most 61 bins (value-width bins,
+//     monotone in v, computed from the value alone).  When f > 0 the
+//     candidates (samples in [lo, hi]) are bucketed by key (count, exclusive
+//     scan, place) and each bucket is sorted by value, so bin b's candidates
+//     are the sorted range [start[b], start[b+1]).
+//  3. fine pass: sweep over the fine keys.  The walk lands every pixel in a bin
+//     b with residual rank r' = R2 - #keys < b; the median is lo + b - 1 when
+//     f = 0, else the r'-th candidate of bin b (in sorted order) inside the
+//     pixel's window.
+// Exact by construction.  If an item has more candidates than fit (CMAX) it
+// is split in halves by rows (down to single rows); a row that still does not
+// fit is selected per pixel by brute force (radix selection over the window)
+// -- only adversarial high-entropy data gets there.
+#include <cstdint>
+#include <cstdlib>
+#include <cuda_runtime.h>
+
+#include "tm_common.cuh"
+#include "tm_kernels.h"
+#include "tm_sweep.cuh"
+
+namespace tmb {
+namespace {
+
+template <typename T, int K>
+struct RankCfg {
+  static constexpr int NB = 64;                        // key bins
+  using SW = WarpSweep<K, NB>;
+  static constexpr int RMAX = 64;
+  static constexpr int G = 4;                          // ring refill group (rows)
+  static constexpr int H = K / 2;
+  static constexpr int FW = 64 + K - 1;                // footprint columns
+  static constexpr int KW = ((FW + 3) / 4) * 4 + 8;    // ring row bytes
+  static constexpr int RING = K + 2 * G + 1;           // ring rows
+  static constexpr int kRingBytes = ((RING * KW + 15) / 16) * 16;
+  static constexpr int CMAX = 4096;                    // candidates per (sub-)item
+  static constexpr int kValBytes = CMAX * (int)sizeof(T);
+  static constexpr int kPosBytes = CMAX * 2;
+  static constexpr int kStartBytes = (NB + 16) * 4 * 2;  // start[] + cursor[]
+  static constexpr int kWarpBytes =
+      SW::kHistBytes + kRingBytes + kValBytes + kPosBytes + kStartBytes;
+  static constexpr int BITS = 8 * (int)sizeof(T);
+  static constexpr int SHIFT = BITS - 6;               // coarse key = top 6 bits
+  static constexpr int E = (G * FW + 31) / 32;         // prefetch samples per lane
+};
+
+template <typename T>
+__device__ __forceinline__ uint32_t load_s(const T* src, const Job& job, int y, int x) {
+  return __ldg(src + (int64_t)y * job.src_pitch + (int64_t)x * job.channels);
+}
+
+// Brute-force exact median of one pixel (last-resort path): MSB-first radix
+// selection over the clamped window, one bit per pass.
+template <typename T, int K>
+__device__ uint32_t brute_median(const T* src, const Job& job, int yc, int xc) {
+  constexpr int R2 = (K * K + 1) / 2;
+  uint32_t prefix = 0, need = R2;
+  for (int bit = 8 * (int)sizeof(T) - 1; bit >= 0; bit--) {
+    const uint32_t hi_mask = bit + 1 >= 32 ? 0u : (~0u << (bit + 1));
+    uint32_t zeros = 0;
+    for (int dy = -K / 2; dy <= K / 2; dy++) {
+      const int y = clampi(yc + dy, 0, job.src_h - 1);
+      for (int dx = -K / 2; dx <= K / 2; dx++) {
+        const uint32_t v = load_s(src, job, y, clampi(xc + dx, 0, job.width - 1));
+        zeros += ((v & hi_mask) == prefix) && !((v >> bit) & 1u);
+      }
+    }
+    if (need > zeros) {
+      need -= zeros;
+      prefix |= 1u << bit;
+    }
+  }
+  return prefix;
+}
+
+// Key of a sample: coarse pass (f < 0): top 6 bits; fine pass: 0 / 63 outside
+// [lo, hi], 1 + ((v - lo) >> f) inside.
+struct KeyFn {
+  uint32_t lo, hi;
+  int f;  // < 0: coarse
+  int shift;
+  __device__ __forceinline__ uint8_t operator()(uint32_t v) const {
+    if (f < 0) return (uint8_t)(v >> shift);
+    return v < lo ? 0 : (v > hi ? 63 : (uint8_t)(1 + ((v - lo) >> f)));
+  }
+};
+
+template <typename T, int K>
+__global__ void __launch_bounds__(32) rank_kernel(Job job, int R, int n_strips, int n_segs) {
+  using C = RankCfg<T, K>;
+  using SW = typename C::SW;
+  extern __shared__ __align__(16) uint32_t smem[];
+  const int lane = threadIdx.x;
+  uint8_t* ring = reinterpret_cast<uint8_t*>(smem) + SW::kHistBytes;
+  T* cval = reinterpret_cast<T*>(ring + C::kRingBytes);                  // bucketed candidates
+  uint16_t* cpos = reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(cval) + C::kValBytes);
+  int* start = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(cpos) + C::kPosBytes);
+  int* cursor = start + C::NB + 16;
+  SW sw;
+  sw.init(smem, lane);
+  const int W = job.width, SH = job.src_h, CH = job.channels;
+  const int n_items = n_strips * CH * n_segs;
+
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const int chan = item % CH;
+    const int strip = (item / CH) % n_strips;
+    const int seg = item / (CH * n_strips);
+    const int X0 = strip * 64;
+    const int Yi = seg * R;
+    const int rows_item = min(R, job.out_h - Yi);
+    const T* src = static_cast<const T*>(job.src) + chan;
+    T* dst = static_cast<T*>(job.dst) + chan;
+    const int x = X0 + 2 * lane;
+
+    int Rcur = rows_item;
+    for (int y0 = 0; y0 < rows_item;) {
+      const int rows = min(Rcur, rows_item - y0);
+      const int Y0 = Yi + y0;
+      const int sy_base = job.out_y0 + Y0 - C::H;  // source row of footprint row 0
+      const int q_end = K + rows - 1;              // footprint rows
+
+      // One sweep over the item with keys from `kf`; `emit(t)` after each row.
+      auto sweep = [&](const KeyFn& kf, auto&& emit) {
+        auto fetch = [&](int q0, uint8_t (&v)[C::E]) {
+#pragma unroll
+          for (int e = 0; e < C::E; e++) {
+            const int idx = lane + e * 32;
+            const int g = idx / C::FW, c = idx - (idx / C::FW) * C::FW;
+            if (idx < C::G * C::FW && q0 + g < q_end)
+              v[e] = kf(load_s(src, job, clampi(sy_base + q0 + g, 0, SH - 1),
+                               clampi(X0 - C::H + c, 0, W - 1)));
+          }
+        };
+        auto stash = [&](int q0, const uint8_t (&v)[C::E]) {
+#pragma unroll
+          for (int e = 0; e < C::E; e++) {
+            const int idx = lane + e * 32;
+            const int g = idx / C::FW, c = idx - (idx / C::FW) * C::FW;
+            if (idx < C::G * C::FW && q0 + g < q_end) ring[((q0 + g) % C::RING) * C::KW + c] = v[e];
+          }
+        };
+        auto row = [&](int q) { return ring + (q % C::RING) * C::KW; };
+        __syncwarp();
+        for (int q = 0; q < K + C::G; q += C::G) {
+          uint8_t v[C::E];
+          fetch(q, v);
+          stash(q, v);
+        }
+        sw.zero();
+        __syncwarp();
+        for (int q = 0; q < K; q++) {
+          uint32_t ch[SW::NC];
+          SW::chunks(row(q), lane, ch);
+          sw.add_row(ch);
+        }
+        sw.init_median();
+        emit(0);
+        for (int t0 = 1; t0 < rows; t0 += C::G) {
+          uint8_t nxt[C::E];
+          const int qn = K + t0 - 1 + C::G;
+          if (qn < q_end) fetch(qn, nxt);
+          const int t1 = min(t0 + C::G, rows);
+          for (int t = t0; t < t1; t++) {
+            uint32_t co[SW::NC], ci[SW::NC];
+            SW::chunks(row(t - 1), lane, co);
+            SW::chunks(row(t - 1 + K), lane, ci);
+            sw.step(co, ci);
+            emit(t);
+          }
+          if (qn < q_end) stash(qn, nxt);
+          __syncwarp();
+        }
+      };
+
+      // ---- 1. coarse pass on the top 6 bits --------------------------------
+      int blo = C::NB - 1, bhi = 0;
+      {
+        KeyFn kf{0u, 0u, -1, C::SHIFT};
+        sweep(kf, [&](int) {
+          if (x < W) {
+            blo = min(blo, sw.m[0]);
+            bhi = max(bhi, sw.m[0]);
+          }
+          if (x + 1 < W) {
+            blo = min(blo, sw.m[1]);
+            bhi = max(bhi, sw.m[1]);
+          }
+        });
+      }
+      for (int o = 16; o; o >>= 1) {
+        blo = min(blo, __shfl_xor_sync(0xffffffffu, blo, o));
+        bhi = max(bhi, __shfl_xor_sync(0xffffffffu, bhi, o));
+      }
+      const uint32_t lo = (uint32_t)blo << C::SHIFT;
+      const uint32_t hi = (uint32_t)(((uint64_t)(bhi + 1) << C::SHIFT) - 1);
+      int f = 0;
+      while (((hi - lo) >> f) > (uint32_t)(C::NB - 3)) f++;
+      const KeyFn kf{lo, hi, f, 0};
+
+      // ---- 2. candidates bucketed by fine key (only when f > 0) ----------
+      int n_cand = 0;
+      // Two scans of the footprint: count per key, then place each candidate
+      // at its bucket's cursor; each bucket is then sorted by value.
+      if (f > 0) {
+        for (int b = lane; b < C::NB + 16; b += 32) start[b] = 0;
+        __syncwarp();
+        auto scan = [&](auto&& visit) {
+          for (int q0 = 0; q0 < q_end; q0 += C::G) {
+            uint32_t v[C::E];
+#pragma unroll
+            for (int e = 0; e < C::E; e++) {
+              const int idx = lane + e * 32;
+              const int g = idx / C::FW, c = idx - (idx / C::FW) * C::FW;
+              v[e] = (idx < C::G * C::FW && q0 + g < q_end)
+                         ? load_s(src, job, clampi(sy_base + q0 + g, 0, SH - 1),
+                                  clampi(X0 - C::H + c, 0, W - 1))
+                         : 0xFFFFFFFFu;
+            }
+#pragma unroll
+            for (int e = 0; e < C::E; e++) {
+              const int idx = lane + e * 32;
+              const int g = idx / C::FW, c = idx - (idx / C::FW) * C::FW;
+              if (idx < C::G * C::FW && q0 + g < q_end && v[e] >= lo && v[e] <= hi)
+                visit(v[e], (uint32_t)(((q0 + g) << 8) | c));
+            }
+          }
+        };
+        scan([&](uint32_t v, uint32_t) { atomicAdd(&start[kf(v)], 1); });
+        __syncwarp();
+        // exclusive scan of the 64 bucket counts (2 per lane)
+        const int c0 = start[2 * lane], c1 = start[2 * lane + 1];
+        int incl = c0 + c1;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        n_cand = __shfl_sync(0xffffffffu, incl, 31);
+        __syncwarp();
+        start[2 * lane] = incl - c0 - c1;
+        start[2 * lane + 1] = incl - c1;
+        cursor[2 * lane] = incl - c0 - c1;
+        cursor[2 * lane + 1] = incl - c1;
+        if (lane == 0) start[C::NB] = n_cand;
+        __syncwarp();
+        if (n_cand > C::CMAX) {
+          if (rows > 1) {  // too many candidates: halve the sub-item
+            Rcur = (rows + 1) / 2;
+            continue;
+          }
+          for (int c = 0; c < 2; c++)  // a single row that still does not fit
+            if (x + c < W)
+              dst[(int64_t)Y0 * job.dst_pitch + (int64_t)(x + c) * CH] =
+                  (T)brute_median<T, K>(src, job, job.out_y0 + Y0, x + c);
+          y0 += rows;
+          Rcur = rows_item;
+          continue;
+        }
+        scan([&](uint32_t v, uint32_t p) {
+          const int slot = atomicAdd(&cursor[kf(v)], 1);
+          cval[slot] = (T)v;
+          cpos[slot] = (uint16_t)p;
+        });
+        __syncwarp();
+        // sort each bucket by value: insertion sort per lane for small
+        // buckets, the whole warp (odd-even transposition) for large ones
+        for (int b = 1 + lane; b < C::NB - 1; b += 32) {
+          const int i0 = start[b], i1 = start[b + 1];
+          if (i1 - i0 > 64) continue;
+          for (int i = i0 + 1; i < i1; i++) {
+            const T v = cval[i];
+            const uint16_t p = cpos[i];
+            int j = i - 1;
+            while (j >= i0 && cval[j] > v) {
+              cval[j + 1] = cval[j];
+              cpos[j + 1] = cpos[j];
+              j--;
+            }
+            cval[j + 1] = v;
+            cpos[j + 1] = p;
+          }
+        }
+        __syncwarp();
+        for (int b = 1; b < C::NB - 1; b++) {
+          const int i0 = start[b], n = start[b + 1] - i0;
+          if (n <= 64) continue;
+          for (int ph = 0; ph < n; ph++) {
+            for (int i = i0 + (ph & 1) + 2 * lane; i + 1 < i0 + n; i += 64) {
+              const T a = cval[i], c = cval[i + 1];
+              if (a > c) {
+                const uint16_t pa = cpos[i];
+                cval[i] = c;
+                cval[i + 1] = a;
+                cpos[i] = cpos[i + 1];
+                cpos[i + 1] = pa;
+              }
+            }
+            __syncwarp();
+          }
+        }
+      }
+
+      // ---- 3. fine pass -----------------------------------------------------
+      sweep(kf, [&](int t) {
+#pragma unroll
+        for (int c = 0; c < 2; c++) {
+          const int b = sw.m[c];
+          uint32_t v = 0;
+          if (b < 1 || b > C::NB - 2) {
+            // only columns beyond the image edge (excluded from [lo, hi]) land here
+          } else if (f == 0) {
+            v = lo + (uint32_t)(b - 1);
+          } else {
+            // r'-th in-window candidate of bin b, in sorted order
+            int need = SW::R2 - sw.bl[c];
+            const int cx = 2 * lane + c;  // window columns [cx, cx + K), rows [t, t + K)
+            for (int i = start[b], i1 = start[b + 1]; i < i1; i++) {
+              const uint32_t p = cpos[i];
+              const int pq = (int)(p >> 8) - t, pc = (int)(p & 0xFF) - cx;
+              if ((unsigned)pq < (unsigned)K && (unsigned)pc < (unsigned)K && --need == 0) {
+                v = cval[i];
+                break;
+              }
+            }
+          }
+          if (x + c < W) dst[(int64_t)(Y0 + t) * job.dst_pitch + (int64_t)(x + c) * CH] = (T)v;
+        }
+      });
+      y0 += rows;
+      Rcur = rows_item;
+    }
+  }
+}
+
+template <typename T, int K>
+int launch_rank_k(const Job& job, cudaStream_t stream) {
+  using C = RankCfg<T, K>;
+  constexpr int kSmem = C::kWarpBytes;
+  static_assert(kSmem <= 227 * 1024, "rank kernel does not fit in shared memory");
+  auto fn = rank_kernel<T, K>;
+  static int occ = -1;
+  static int sms = 0;
+  if (occ < 0) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    if (e != cudaSuccess) return (int)e;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int o = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, 32, kSmem);
+    occ = o > 0 ? o : 1;
+  }
+  const int n_strips = (job.width + 63) / 64;
+  const long slots = (long)sms * occ;
+  int best_R = C::RMAX;
+  long best_cost = 0x7fffffffffffL;
+  for (int R = 8; R <= C::RMAX; R *= 2) {
+    const long segs = (job.out_h + R - 1) / R;
+    const long items = segs * n_strips * job.channels;
+    const long waves = (items + slots - 1) / slots;
+    const long cost = waves * (long)(min(R, job.out_h) + K + 8);
+    if (cost < best_cost) {
+      best_cost = cost;
+      best_R = R;
+    }
+    if (R >= job.out_h) break;
+  }
+  const int R = best_R;
+  const int n_segs = (job.out_h + R - 1) / R;
+  const long items = (long)n_segs * n_strips * job.channels;
+  const int grid = (int)(items < slots ? items : slots);
+  fn<<<grid, 32, kSmem, stream>>>(job, R, n_strips, n_segs);
+  return (int)cudaGetLastError();
+}
+
+template <typename T, int... Ks>
+struct RankTable {
+  static int launch(int k, const Job& job, cudaStream_t s) {
+    int rc = (int)cudaErrorInvalidValue;
+    ((k == Ks ? (rc = launch_rank_k<T, Ks>(job, s), 0) : 0), ...);
+    return rc;
+  }
+};
+
+template <typename T>
+using RankAll = RankTable<T, 3, 5, 7, 9, 11, 13, 15, 17, 19, 21, 23, 25, 27, 29, 31, 33, 35, 37,
+                          39, 41, 43, 45, 47, 49, 51, 53, 55, 57, 59, 61, 63, 65, 67, 69, 71, 73,
+                          75>;
+
+}  // namespace
+
+bool rank_supports(int bits, int k) {
+  return (bits == 16 || bits == 32) && k >= 3 && k <= 75 && (k & 1);
+}
+
+int launch_rank(int bits, const Job& job, int k, cudaStream_t s) {
+  if (!rank_supports(bits, k)) return (int)cudaErrorInvalidValue;
+  return bits == 16 ? RankAll<uint16_t>::launch(k, job, s) : RankAll<uint32_t>::launch(k, job, s);
+}
+
+}  // namespace tmb

@@ -1,0 +1,182 @@
+// tm_sweep.cuh -- the warp-level sliding-histogram sweep shared by the data-
+// aware kernels (tm_hist.cu: 8-bit samples, NB = 256 bins; tm_rank.cu: 6-bit
+// keys derived from 16/32-bit samples, NB = 64).
+//
+// One warp owns 64 adjacent output columns; lane l owns columns 2l and 2l+1,
+// whose 256-bin histograms share storage: bin v of column 2l is the low
+// half-word, of column 2l+1 the high half-word of one 32-bit word.  A key at
+// window column j (0..K relative to column 2l) belongs to column 2l's window
+// when j < K and to 2l+1's when j > 0, so its update is ONE shared-memory
+// atomic add of the compile-time constant 0x1 / 0x10001 / 0x10000 (RED.ADD:
+// no return, no read-modify-write round trip).  Counts are at most K^2 < 2^16
+// and never negative, so the halves never carry into each other.
+//
+// Histogram words: bins -kPad .. NB - 1 + kPad (zero padding for the 8-bin walk)
+// x 32 lanes, word (bin, lane) at bin * 32 + lane -- a warp's accesses hit 32
+// distinct banks whatever the bins.
+//
+// Median tracking per column: m = bin holding rank R2, bl = #keys < m.  A row
+// step applies the leaving and entering rows, updates bl with SIMD byte
+// compares (__vsetltu4: 4 keys per instruction) and walks m up to 8 bins per
+// round trip; the walk is warp-convergent (a converged lane's step is
+// idempotent, so the lanes loop until all agree).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tmb {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// Histogram traffic is explicit PTX (RED for updates, volatile loads/stores
+// otherwise), so no compiler pass reorders accesses that alias through
+// data-dependent bin addresses.
+__device__ __forceinline__ void red_add(uint32_t a, uint32_t v) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_hist(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_hist(uint32_t a, uint32_t v) {
+  asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
+template <int K, int NB = 256>
+struct WarpSweep {
+  static constexpr int NS = K + 1;          // keys per lane per row
+  static constexpr int NC = (NS + 3) / 4;   // 4-key chunks
+  static constexpr int NWD = NC + 1;        // aligned words covering the chunks
+  static constexpr int kPad = 8;            // zero bins below 0 / above NB - 1
+  static constexpr int kWords = NB + 2 * kPad;
+  static constexpr int kHistBytes = kWords * 32 * 4;
+  static constexpr int R2 = (K * K + 1) / 2;  // median rank, 1-based
+  static constexpr uint32_t kBinStride = 4u * 32;
+
+  __host__ __device__ static constexpr uint32_t mask_lo(int i) {
+    uint32_t m = 0;
+    for (int b = 0; b < 4; b++)
+      if (4 * i + b < K) m |= 0x01u << (8 * b);
+    return m;
+  }
+  __host__ __device__ static constexpr uint32_t mask_hi(int i) {
+    uint32_t m = 0;
+    for (int b = 0; b < 4; b++)
+      if (4 * i + b >= 1 && 4 * i + b <= K) m |= 0x01u << (8 * b);
+    return m;
+  }
+  __host__ __device__ static constexpr uint32_t inc(int j) {
+    return j == 0 ? 0x1u : (j == K ? 0x10000u : 0x10001u);
+  }
+
+  uint32_t hb;  // shared address of bin 0 of this lane
+  int m[2], bl[2];
+
+  // `hist` = the warp's kHistBytes region.
+  __device__ __forceinline__ void init(uint32_t* hist, int lane) {
+    hb = smem_u32(hist + kPad * 32 + lane);
+  }
+  __device__ __forceinline__ void zero() {
+    for (int b = -kPad; b < NB + kPad; b++) st_hist(hb + b * kBinStride, 0u);
+  }
+  // Keys 0..K of a byte row for this lane (row columns 2*lane .. 2*lane + K),
+  // `row` 4-byte aligned, at least 2*32 + K + 8 bytes long.
+  __device__ __forceinline__ static void chunks(const uint8_t* row, int lane, uint32_t (&ch)[NC]) {
+    const uint32_t* wp = reinterpret_cast<const uint32_t*>(row) + (lane >> 1);
+    const int sh = 16 * (lane & 1);
+    uint32_t w[NWD];
+#pragma unroll
+    for (int i = 0; i < NWD; i++) w[i] = wp[i];
+#pragma unroll
+    for (int i = 0; i < NC; i++) ch[i] = __funnelshift_r(w[i], w[i + 1], sh);
+  }
+  __device__ __forceinline__ uint32_t addr_of(const uint32_t (&ch)[NC], int j) const {
+    return hb + __byte_perm(ch[j >> 2], 0u, 0x4440 | (j & 3)) * kBinStride;
+  }
+  __device__ __forceinline__ void add_row(const uint32_t (&ch)[NC]) {
+#pragma unroll
+    for (int j = 0; j <= K; j++) red_add(addr_of(ch, j), inc(j));
+  }
+  __device__ __forceinline__ int count(int b, int c) const {
+    return (int)((ld_hist(hb + b * kBinStride) >> (16 * c)) & 0xFFFFu);
+  }
+  // After the K-row build: start both columns at bin NB / 2.
+  __device__ __forceinline__ void init_median() {
+#pragma unroll
+    for (int c = 0; c < 2; c++) {
+      int acc = 0;
+      for (int b = 0; b < NB / 2; b++) acc += count(b, c);
+      m[c] = NB / 2;
+      bl[c] = acc;
+    }
+    walk();
+  }
+  // Slide the window one row: `co` leaves, `ci` enters.
+  __device__ __forceinline__ void step(const uint32_t (&co)[NC], const uint32_t (&ci)[NC]) {
+#pragma unroll
+    for (int j = 0; j <= K; j++) {
+      red_add(addr_of(co, j), 0u - inc(j));
+      red_add(addr_of(ci, j), inc(j));
+    }
+    // bl[c] += #entering < m[c] - #leaving < m[c] (before m moves)
+#pragma unroll
+    for (int c = 0; c < 2; c++) {
+      const uint32_t mb = (uint32_t)m[c] * 0x01010101u;
+      uint32_t ai = 0, ao = 0;
+#pragma unroll
+      for (int i = 0; i < NC; i++) {
+        const uint32_t mk = c ? mask_hi(i) : mask_lo(i);
+        ai += __vsetltu4(ci[i], mb) & mk;
+        ao += __vsetltu4(co[i], mb) & mk;
+      }
+      bl[c] += (int)__dp4a(ai, 0x01010101u, 0u) - (int)__dp4a(ao, 0x01010101u, 0u);
+    }
+    walk();
+  }
+  // Move m[c] to the bin holding rank R2, 8 bins per round trip.
+  __device__ __forceinline__ void walk() {
+    constexpr int S = 8;
+    for (;;) {
+      bool fin[2];
+#pragma unroll
+      for (int c = 0; c < 2; c++) {
+        const bool down = bl[c] >= R2;
+        const int s1 = down ? -1 : 1;
+        const uint32_t a0 = hb + (uint32_t)(down ? m[c] - 1 : m[c]) * kBinStride;
+        const uint32_t da = down ? (uint32_t)(-(int)kBinStride) : kBinStride;
+        int t[S];
+        int acc = bl[c];
+        int nlt = 0, best = down ? -1 : bl[c];
+#pragma unroll
+        for (int i = 0; i < S; i++) {
+          const int h = (int)((ld_hist(a0 + i * da) >> (16 * c)) & 0xFFFFu);
+          acc += s1 * h;
+          t[i] = acc;
+        }
+#pragma unroll
+        for (int i = 0; i < S; i++) {
+          const bool lt = t[i] < R2;
+          nlt += lt;
+          best = lt ? max(best, t[i]) : best;  // largest prefix still below rank
+        }
+        // up: bins m .. m+nlt-1 lie wholly below rank R2 -> median in m + nlt;
+        // down: the first bin whose prefix drops below R2 is m - (S-nlt) - 1.
+        const int nge = S - nlt;
+        if (down) {
+          fin[c] = nlt > 0;
+          m[c] -= fin[c] ? nge + 1 : S;
+        } else {
+          fin[c] = nlt < S;
+          m[c] += nlt;
+        }
+        bl[c] = fin[c] ? best : t[S - 1];
+      }
+      if (__all_sync(0xffffffffu, fin[0] && fin[1])) break;
+    }
+  }
+};
+
+}  // namespace tmb

@@ -86,3 +86,47 @@ def test_histogram_u8_tall_image_many_segments():
     img = generate(TestImageSpec("random", 140, 3000, 8, seed=9))
     for k in (7, 25):
         assert np.array_equal(run_forced("histogram", img, k), oracle_median_filter_c(img, k)), k
+
+
+RANK_KS = [3, 9, 17, 29, 33, 47, 75]
+
+
+@pytest.mark.parametrize("bits", [16, 32])
+@pytest.mark.parametrize("k", RANK_KS)
+def test_rank_patterns(bits, k):
+    for name, img in images(bits, 157, 301, seed=k):
+        assert np.array_equal(run_forced("rank", img, k), oracle_median_filter_c(img, k)), (bits, name, k)
+
+
+@pytest.mark.parametrize("bits", [16, 32])
+@pytest.mark.parametrize("shape", [(1, 1), (1, 200), (200, 1), (3, 5), (130, 129), (257, 300)])
+def test_rank_shapes(bits, shape):
+    rng = np.random.default_rng(shape[0] * 1000 + shape[1] + bits)
+    dt = {16: np.uint16, 32: np.uint32}[bits]
+    img = rng.integers(0, np.iinfo(dt).max, size=shape, dtype=dt, endpoint=True)
+    for k in (3, 17, 41):
+        assert np.array_equal(run_forced("rank", img, k), oracle_median_filter_c(img, k)), (shape, k)
+
+
+@pytest.mark.parametrize("bits", [16, 32])
+def test_rank_high_entropy_narrow_band(bits):
+    """Many distinct candidates in a narrow value band: rank bins + fine scan,
+    and the candidate-overflow split (smooth ramp + small noise)."""
+    rng = np.random.default_rng(bits)
+    dt = {16: np.uint16, 32: np.uint32}[bits]
+    h, w = 150, 260
+    ramp = np.linspace(1000, 1200 if bits == 16 else 5000, w)[None, :] + np.zeros((h, 1))
+    scale = 1 if bits == 16 else 1 << 12
+    img = ((ramp + rng.integers(0, 300, size=(h, w))) * scale).astype(dt)
+    for k in (29, 51):
+        assert np.array_equal(run_forced("rank", img, k), oracle_median_filter_c(img, k)), k
+
+
+def test_rank_interleaved_planes_u16():
+    rng = np.random.default_rng(6)
+    img = rng.integers(0, 65536, (90, 170, 3), dtype=np.uint16)
+    for k in (9, 31):
+        out = run_forced("rank", img, k)
+        for c in range(3):
+            ref = oracle_median_filter_c(np.ascontiguousarray(img[..., c]), k)
+            assert np.array_equal(out[..., c], ref), (k, c)
