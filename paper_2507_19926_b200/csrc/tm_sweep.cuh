@@ -1,6 +1,6 @@
 // tm_sweep.cuh -- the warp-level sliding-histogram sweep shared by the data-
-// aware kernels (tm_hist.cu: 8-bit samples, NB = 256 bins; tm_rank.cu: 6-bit
-// keys derived from 16/32-bit samples, NB = 64).
+// aware kernels (tm_hist.cu: 8-bit samples, NB = 256 bins; tm_rank.cu: 7-bit
+// keys derived from 16/32-bit samples, NB = 128).
 //
 // One warp owns 64 adjacent output columns; lane l owns columns 2l and 2l+1,
 // whose 256-bin histograms share storage: bin v of column 2l is the low
