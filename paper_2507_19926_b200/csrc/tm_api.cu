@@ -1,5 +1,6 @@
 // tm_api.cu -- the C ABI (include/tilemedian_b200.h): validation, dispatch,
 // launch accounting and the host-buffer entry point.
+#include <algorithm>
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
@@ -40,7 +41,7 @@ bool supports(int kernel, int bits, int kw, int kh) {
   const bool square = kw == kh;
   switch (kernel) {
     case TM_KERNEL_OBLIVIOUS: return square && find_obl(bits, kw) != nullptr;
-    case TM_KERNEL_AWARE: return square && kw >= 9;
+    case TM_KERNEL_MULTIPASS: return square && kw >= 9;
     case TM_KERNEL_SELECT: return true;
     case TM_KERNEL_HISTOGRAM: return square && bits == 8 && tmb::hist8_supports(kw);
     case TM_KERNEL_RANK: return square && tmb::rank_supports(bits, kw);
@@ -48,31 +49,36 @@ bool supports(int kernel, int bits, int kw, int kh) {
   }
 }
 
-// The fastest exact kernel for (bits, k) on B200, from measured sweeps
-// (profiles/).
-int best_aware(int bits, int k) {
+// The data-aware kernel for (bits, k): sliding histograms of the samples for
+// 8-bit data, of 7-bit keys (coarse + candidate passes) for 16/32-bit data.
+int aware_kernel(int bits, int k) {
   if (bits == 8 && tmb::hist8_supports(k)) return TM_KERNEL_HISTOGRAM;
   if (tmb::rank_supports(bits, k)) return TM_KERNEL_RANK;
-  return TM_KERNEL_AWARE;
+  return TM_KERNEL_MULTIPASS;
+}
+
+// "auto": the fastest exact kernel per (bits, k), measured on B200 over the
+// full k = 3..75 sweep of 4096^2 images (profiles/r01_sweep_4096_all_kernels
+// .jsonl): the oblivious network up to the crossover, the data-aware kernel
+// from it on.  Crossovers: 8-bit k = 15, 16-bit k = 29, 32-bit k = 27.
+int auto_kernel(int bits, int k) {
+  const int crossover = bits == 8 ? 15 : (bits == 16 ? 29 : 27);
+  if (k < crossover && find_obl(bits, k)) return TM_KERNEL_OBLIVIOUS;
+  return aware_kernel(bits, k);
 }
 
 int route(int bits, int kw, int kh, int variant) {
   if (g_force && supports(g_force, bits, kw, kh)) return g_force;
   const bool square = kw == kh;
-  // 8-bit data: the sliding-histogram kernel overtakes the oblivious network
-  // from k = 15 on (profiles/r01_sweep_4096_hist.jsonl).
-  const bool obl = square && find_obl(bits, kw) != nullptr &&
-                   !(bits == 8 && kw >= 15 && tmb::hist8_supports(kw));
   switch (variant) {
     case TM_VARIANT_ORACLE:
       return TM_KERNEL_SELECT;
     case TM_VARIANT_OBLIVIOUS:
       return (square && find_obl(bits, kw)) ? TM_KERNEL_OBLIVIOUS : TM_KERNEL_SELECT;
     case TM_VARIANT_AWARE:
-      return (square && kw >= 9) ? best_aware(bits, kw) : TM_KERNEL_SELECT;
+      return (square && kw >= 9) ? aware_kernel(bits, kw) : TM_KERNEL_SELECT;
     default:  // auto
-      if (obl) return TM_KERNEL_OBLIVIOUS;
-      return (square && kw >= 9) ? best_aware(bits, kw) : TM_KERNEL_SELECT;
+      return square ? auto_kernel(bits, kw) : TM_KERNEL_SELECT;
   }
 }
 
@@ -127,7 +133,7 @@ int tm_median2d_band(const void* src, int64_t src_pitch, int32_t src_rows, int32
     case TM_KERNEL_OBLIVIOUS:
       err = find_obl(bits, k_w)->fn(job, s);
       break;
-    case TM_KERNEL_AWARE:
+    case TM_KERNEL_MULTIPASS:
       err = tmb::launch_aware(bits, job, k_w, s);
       break;
     case TM_KERNEL_HISTOGRAM:
@@ -175,10 +181,16 @@ int tm_median2d_host(const void* src, int64_t src_pitch, void* dst, int64_t dst_
   if (channels < 1) return fail(TM_EINVAL, "bad channel count %d", channels);
   const int64_t row = (int64_t)width * channels * (bits / 8);
   if (src_pitch < row || dst_pitch < row) return fail(TM_EINVAL, "pitch smaller than a row");
+  // Row bands pipelined over three streams: band b's H2D copy, band b-1's
+  // filter and band b-2's D2H copy run concurrently (PCIe is full duplex), so
+  // the call costs about max(H2D, filter, D2H) instead of their sum.  A band's
+  // filter waits for the input chunk holding its last halo row.
+  constexpr int kMaxBands = 16;
   struct Scratch {
     void* buf = nullptr;
     size_t bytes = 0;
-    cudaStream_t stream = nullptr;
+    cudaStream_t st[3] = {nullptr, nullptr, nullptr};  // h2d, filter, d2h
+    cudaEvent_t ev_in[kMaxBands] = {}, ev_out[kMaxBands] = {};
   };
   static thread_local std::vector<Scratch> per_dev;
   if (device < 0) return fail(TM_EINVAL, "bad device %d", device);
@@ -195,20 +207,55 @@ int tm_median2d_host(const void* src, int64_t src_pitch, void* dst, int64_t dst_
     if (e != cudaSuccess) return fail(TM_ECUDA, "cudaMalloc: %s", cudaGetErrorString(e));
     sc.bytes = need;
   }
-  if (!sc.stream) {
-    e = cudaStreamCreateWithFlags(&sc.stream, cudaStreamNonBlocking);
-    if (e != cudaSuccess) return fail(TM_ECUDA, "cudaStreamCreate: %s", cudaGetErrorString(e));
+  if (!sc.st[0]) {
+    for (auto& st : sc.st) {
+      e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+      if (e != cudaSuccess) return fail(TM_ECUDA, "cudaStreamCreate: %s", cudaGetErrorString(e));
+    }
+    for (int b = 0; b < kMaxBands; b++) {
+      e = cudaEventCreateWithFlags(&sc.ev_in[b], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&sc.ev_out[b], cudaEventDisableTiming);
+      if (e != cudaSuccess) return fail(TM_ECUDA, "cudaEventCreate: %s", cudaGetErrorString(e));
+    }
   }
   char* din = static_cast<char*>(sc.buf);
   char* dout = din + (size_t)row * height;
-  e = cudaMemcpy2DAsync(din, row, src, src_pitch, row, height, cudaMemcpyHostToDevice, sc.stream);
-  if (e != cudaSuccess) return fail(TM_ECUDA, "H2D copy: %s", cudaGetErrorString(e));
-  rc = tm_median2d_band(din, row, height, 0, height, dout, row, width, channels, bits, k_w, k_h,
-                        variant, sc.stream);
-  if (rc) return rc;
-  e = cudaMemcpy2DAsync(dst, dst_pitch, dout, row, row, height, cudaMemcpyDeviceToHost, sc.stream);
-  if (e != cudaSuccess) return fail(TM_ECUDA, "D2H copy: %s", cudaGetErrorString(e));
-  e = cudaStreamSynchronize(sc.stream);
+  const int halo = k_h / 2;
+  // bands of >= 128 rows, at most kMaxBands
+  const int nb = std::max(1, std::min(kMaxBands, height / 128));
+  int y[kMaxBands + 1];
+  for (int b = 0; b <= nb; b++) y[b] = (int)((int64_t)height * b / nb);
+  const char* hsrc = static_cast<const char*>(src);
+  char* hdst = static_cast<char*>(dst);
+  for (int b = 0; b < nb; b++) {
+    e = cudaMemcpy2DAsync(din + (size_t)y[b] * row, row, hsrc + (int64_t)y[b] * src_pitch,
+                          src_pitch, row, y[b + 1] - y[b], cudaMemcpyHostToDevice, sc.st[0]);
+    if (e == cudaSuccess) e = cudaEventRecord(sc.ev_in[b], sc.st[0]);
+    if (e != cudaSuccess) return fail(TM_ECUDA, "H2D copy: %s", cudaGetErrorString(e));
+  }
+  int have = -1;  // newest input chunk the filter stream already waits for
+  for (int b = 0; b < nb; b++) {
+    const int last_src = std::min(height, y[b + 1] + halo) - 1;
+    int chunk = b;
+    while (chunk + 1 < nb && y[chunk + 1] <= last_src) chunk++;
+    if (chunk > have) {
+      e = cudaStreamWaitEvent(sc.st[1], sc.ev_in[chunk], 0);
+      if (e != cudaSuccess) return fail(TM_ECUDA, "stream wait: %s", cudaGetErrorString(e));
+      have = chunk;
+    }
+    rc = tm_median2d_band(din, row, height, y[b], y[b + 1] - y[b], dout + (size_t)y[b] * row, row,
+                          width, channels, bits, k_w, k_h, variant, sc.st[1]);
+    if (rc) return rc;
+    e = cudaEventRecord(sc.ev_out[b], sc.st[1]);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(sc.st[2], sc.ev_out[b], 0);
+    if (e == cudaSuccess)
+      e = cudaMemcpy2DAsync(hdst + (int64_t)y[b] * dst_pitch, dst_pitch, dout + (size_t)y[b] * row,
+                            row, row, y[b + 1] - y[b], cudaMemcpyDeviceToHost, sc.st[2]);
+    if (e != cudaSuccess) return fail(TM_ECUDA, "D2H copy: %s", cudaGetErrorString(e));
+  }
+  e = cudaStreamSynchronize(sc.st[2]);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(sc.st[1]);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(sc.st[0]);
   if (e != cudaSuccess) return fail(TM_ECUDA, "kernel failed: %s", cudaGetErrorString(e));
   return TM_OK;
 }
@@ -221,7 +268,7 @@ int tm_dispatch_query(int32_t bits, int32_t k_w, int32_t k_h, int32_t variant) {
 const char* tm_kernel_name(int32_t kernel) {
   switch (kernel) {
     case TM_KERNEL_OBLIVIOUS: return "oblivious";
-    case TM_KERNEL_AWARE: return "aware";
+    case TM_KERNEL_MULTIPASS: return "multipass";
     case TM_KERNEL_SELECT: return "select";
     case TM_KERNEL_HISTOGRAM: return "histogram";
     case TM_KERNEL_RANK: return "rank";

@@ -137,6 +137,13 @@ struct WarpSweep {
     walk();
   }
   // Move m[c] to the bin holding rank R2, 8 bins per round trip.
+  //   up   (bl < R2):  prefix P_i = h(m) + .. + h(m+i); bins m .. m+i lie
+  //                    wholly below rank R2 iff P_i <= X = R2 - 1 - bl;
+  //                    with n = #{P_i <= X}: median bin m + n, bl += P_{n-1}.
+  //   down (bl >= R2): P_i = h(m-1) + .. + h(m-1-i); bin m-1-i still holds
+  //                    rank R2 or above iff P_i <= X = bl - R2; median bin
+  //                    m - 1 - n, bl -= P_n.
+  // n = 8 means keep going (m += / -= 8, bl +/-= P_7).
   __device__ __forceinline__ void walk() {
     constexpr int S = 8;
     for (;;) {
@@ -144,35 +151,33 @@ struct WarpSweep {
 #pragma unroll
       for (int c = 0; c < 2; c++) {
         const bool down = bl[c] >= R2;
-        const int s1 = down ? -1 : 1;
         const uint32_t a0 = hb + (uint32_t)(down ? m[c] - 1 : m[c]) * kBinStride;
         const uint32_t da = down ? (uint32_t)(-(int)kBinStride) : kBinStride;
-        int t[S];
-        int acc = bl[c];
-        int nlt = 0, best = down ? -1 : bl[c];
+        const int X = down ? bl[c] - R2 : R2 - 1 - bl[c];
+        int P[S];
+        int acc = 0;
 #pragma unroll
         for (int i = 0; i < S; i++) {
-          const int h = (int)((ld_hist(a0 + i * da) >> (16 * c)) & 0xFFFFu);
-          acc += s1 * h;
-          t[i] = acc;
+          const uint32_t w = ld_hist(a0 + i * da);
+          acc += (int)(c ? (w >> 16) : (w & 0xFFFFu));
+          P[i] = acc;
         }
+        int n = 0, pin = 0, pout = P[S - 1];  // pin = P_{n-1} (0), pout = P_n (P_7)
 #pragma unroll
-        for (int i = 0; i < S; i++) {
-          const bool lt = t[i] < R2;
-          nlt += lt;
-          best = lt ? max(best, t[i]) : best;  // largest prefix still below rank
+        for (int i = S - 1; i >= 0; i--) {
+          const bool le = P[i] <= X;
+          n += le;
+          pin = (le && pin == 0) ? P[i] : pin;    // largest P_i <= X (P monotone)
+          pout = le ? pout : P[i];                // smallest P_i > X
         }
-        // up: bins m .. m+nlt-1 lie wholly below rank R2 -> median in m + nlt;
-        // down: the first bin whose prefix drops below R2 is m - (S-nlt) - 1.
-        const int nge = S - nlt;
+        fin[c] = n < S;
         if (down) {
-          fin[c] = nlt > 0;
-          m[c] -= fin[c] ? nge + 1 : S;
+          m[c] -= fin[c] ? n + 1 : S;
+          bl[c] -= pout;
         } else {
-          fin[c] = nlt < S;
-          m[c] += nlt;
+          m[c] += n;
+          bl[c] += pin;
         }
-        bl[c] = fin[c] ? best : t[S - 1];
       }
       if (__all_sync(0xffffffffu, fin[0] && fin[1])) break;
     }

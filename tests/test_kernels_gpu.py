@@ -130,3 +130,12 @@ def test_rank_interleaved_planes_u16():
         for c in range(3):
             ref = oracle_median_filter_c(np.ascontiguousarray(img[..., c]), k)
             assert np.array_equal(out[..., c], ref), (k, c)
+
+
+@pytest.mark.parametrize("bits", [8, 16, 32])
+def test_multipass_kernel(bits):
+    """The GPU restatement of the reference's multi-pass aware engine (kept as
+    a forced-only kernel) stays exact."""
+    for name, img in images(bits, 97, 131, seed=bits):
+        for k in (9, 25):
+            assert np.array_equal(run_forced("multipass", img, k), oracle_median_filter_c(img, k)), (name, k)

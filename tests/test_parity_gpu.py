@@ -191,3 +191,25 @@ def test_full_size_bands_vs_oracle(bits, k):
         ref = banded_oracle(img, k, int(y0), int(y1))
         assert np.array_equal(out[y0:y1], ref), (y0, y1)
     # columns at the left/right border are inside every band checked above
+
+
+@pytest.mark.parametrize("bits,k,shape", [(8, 17, (1100, 257, 3)), (16, 41, (900, 190)),
+                                          (32, 75, (530, 97)), (8, 3, (2049, 64))])
+def test_host_entry_point_pipelined_bands(bits, k, shape):
+    """tm_median2d_host splits tall images into row bands pipelined over three
+    streams; halos cross band boundaries (k/2 > band height for k = 75)."""
+    from paper_2507_19926_b200 import _lib
+    lib = _lib.load()
+    dt = {8: np.uint8, 16: np.uint16, 32: np.uint32}[bits]
+    rng = np.random.default_rng(k)
+    img = rng.integers(0, np.iinfo(dt).max, size=shape, dtype=dt, endpoint=True)
+    h, w = shape[:2]
+    ch = shape[2] if len(shape) == 3 else 1
+    out = np.zeros_like(img)
+    rc = lib.tm_median2d_host(img.ctypes.data, img.strides[0], out.ctypes.data, out.strides[0],
+                              w, h, ch, bits, k, k, 0, 0)
+    _lib.check(rc)
+    for c in range(ch):
+        plane = img[..., c] if ch > 1 else img
+        got = out[..., c] if ch > 1 else out
+        assert np.array_equal(got, oracle_median_filter_c(np.ascontiguousarray(plane), k)), c
