@@ -219,7 +219,6 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     from paper_2507_19926_b200 import _lib, bands, filter_planes
-    from paper_2507_19926_b200.engine import pick_variant
     from paper_2507_19926_b200.program import op_model
     lib = _lib.load()
     tdt = {8: torch.uint8, 16: torch.uint16, 32: torch.uint32}[bits]
