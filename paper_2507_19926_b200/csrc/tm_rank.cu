@@ -29,6 +29,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cuda_runtime.h>
+#include <type_traits>
 
 #include "tm_common.cuh"
 #include "tm_kernels.h"
@@ -39,7 +40,12 @@ namespace {
 
 template <typename T, int K>
 struct RankCfg {
-  static constexpr int NB = 128;                       // key bins
+#ifndef TMB_RANK_FINE_BINS
+#define TMB_RANK_FINE_BINS 128
+#endif
+  static constexpr int NBC = 128;                      // coarse key bins (top 7 bits)
+  static constexpr int NB = TMB_RANK_FINE_BINS;        // fine key bins
+  using SWC = WarpSweep<K, NBC>;
   using SW = WarpSweep<K, NB>;
   static constexpr int RMAX = 128;
   static constexpr int G = 4;                          // ring refill group (rows)
@@ -48,14 +54,16 @@ struct RankCfg {
   static constexpr int KW = ((FW + 3) / 4) * 4 + 8;    // ring row bytes
   static constexpr int RING = K + 2 * G + 1;           // ring rows
   static constexpr int kRingBytes = ((RING * KW + 15) / 16) * 16;
-  static constexpr int CMAX = 4096;                    // candidates per (sub-)item
+  // candidates per (sub-)item: the median spread of a 64 x 128 item (and so
+  // the candidate count) grows with k; small k buys occupancy with less
+  static constexpr int CMAX = K <= 45 ? 2048 : 4096;
   static constexpr int kValBytes = CMAX * (int)sizeof(T);
   static constexpr int kPosBytes = CMAX * 2;
   static constexpr int kStartBytes = (NB + 16) * 4;      // start[]
-  static constexpr int kWarpBytes =
-      SW::kHistBytes + kRingBytes + kValBytes + kPosBytes + kStartBytes;
+  static constexpr int kHistBytes = SW::kHistBytes > SWC::kHistBytes ? SW::kHistBytes : SWC::kHistBytes;
+  static constexpr int kWarpBytes = kHistBytes + kRingBytes + kValBytes + kPosBytes + kStartBytes;
   static constexpr int BITS = 8 * (int)sizeof(T);
-  static constexpr int SHIFT = BITS - 7;               // coarse key = top 7 bits
+  static constexpr int SHIFT = BITS - 7;               // coarse key = top 7 bits (NBC)
   static constexpr int E = (G * FW + 31) / 32;         // prefetch samples per lane
 };
 
@@ -118,11 +126,13 @@ __global__ void __launch_bounds__(32) rank_kernel(Job job, int R, int n_strips, 
   using SW = typename C::SW;
   extern __shared__ __align__(16) uint32_t smem[];
   const int lane = threadIdx.x;
-  uint8_t* ring = reinterpret_cast<uint8_t*>(smem) + SW::kHistBytes;
+  uint8_t* ring = reinterpret_cast<uint8_t*>(smem) + C::kHistBytes;
   T* cval = reinterpret_cast<T*>(ring + C::kRingBytes);                  // bucketed candidates
   uint16_t* cpos = reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(cval) + C::kValBytes);
   int* start = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(cpos) + C::kPosBytes);
+  typename C::SWC swc;  // coarse and fine sweeps share the histogram words
   SW sw;
+  swc.init(smem, lane);
   sw.init(smem, lane);
   const int W = job.width, SH = job.src_h, CH = job.channels;
   const int n_items = n_strips * CH * n_segs;
@@ -176,7 +186,8 @@ __global__ void __launch_bounds__(32) rank_kernel(Job job, int R, int n_strips, 
       };
 
       // One sweep over the sub-item with keys from `kf`; `emit(t)` after each row.
-      auto sweep = [&](const KeyFn<C::NB>& kf, auto&& emit) {
+      auto sweep = [&](auto& sw, const auto& kf, auto&& emit) {
+        using S = typename std::remove_reference<decltype(sw)>::type;
         auto stash = [&](int q0, const uint32_t (&v)[C::E]) {
 #pragma unroll
           for (int e = 0; e < C::E; e++) {
@@ -203,8 +214,8 @@ __global__ void __launch_bounds__(32) rank_kernel(Job job, int R, int n_strips, 
         sw.zero();
         __syncwarp();
         for (int q = 0; q < K; q++) {
-          uint32_t ch[SW::NC];
-          SW::chunks(row(q), lane, ch);
+          uint32_t ch[S::NC];
+          S::chunks(row(q), lane, ch);
           sw.add_row(ch);
         }
         sw.init_median();
@@ -215,9 +226,9 @@ __global__ void __launch_bounds__(32) rank_kernel(Job job, int R, int n_strips, 
           if (qn < q_end) fetch_raw(qn, nxt);
           const int t1 = min(t0 + C::G, rows);
           for (int t = t0; t < t1; t++) {
-            uint32_t co[SW::NC], ci[SW::NC];
-            SW::chunks(row(t - 1), lane, co);
-            SW::chunks(row(t - 1 + K), lane, ci);
+            uint32_t co[S::NC], ci[S::NC];
+            S::chunks(row(t - 1), lane, co);
+            S::chunks(row(t - 1 + K), lane, ci);
             sw.step(co, ci);
             emit(t);
           }
@@ -232,16 +243,16 @@ __global__ void __launch_bounds__(32) rank_kernel(Job job, int R, int n_strips, 
       // ---- 1. candidate range: exact coarse pass, or speculative ----------
       uint32_t lo, hi;
       if (exact) {
-        int blo = C::NB - 1, bhi = 0;
-        KeyFn<C::NB> kc{0u, 0u, 0u, -1, C::SHIFT};
-        sweep(kc, [&](int) {
+        int blo = C::NBC - 1, bhi = 0;
+        KeyFn<C::NBC> kc{0u, 0u, 0u, -1, C::SHIFT};
+        sweep(swc, kc, [&](int) {
           if (x < W) {
-            blo = min(blo, sw.m[0]);
-            bhi = max(bhi, sw.m[0]);
+            blo = min(blo, swc.m[0]);
+            bhi = max(bhi, swc.m[0]);
           }
           if (x + 1 < W) {
-            blo = min(blo, sw.m[1]);
-            bhi = max(bhi, sw.m[1]);
+            blo = min(blo, swc.m[1]);
+            bhi = max(bhi, swc.m[1]);
           }
         });
         for (int o = 16; o; o >>= 1) {
@@ -380,7 +391,7 @@ __global__ void __launch_bounds__(32) rank_kernel(Job job, int R, int n_strips, 
       // ---- 3. fine pass -----------------------------------------------------
       bool miss = false;
       uint32_t mlo = kTMax, mhi = 0;
-      sweep(kf, [&](int t) {
+      sweep(sw, kf, [&](int t) {
 #pragma unroll
         for (int c = 0; c < 2; c++) {
           const int b = sw.m[c];
