@@ -332,7 +332,7 @@ def main():
     alu_peak = MINMAX_PEAK_TPS * lanes / 1e12
     hbm_achieved = 2 * esz * per_launch / (kern_ms * 1e-3) / 1e9
     traffic = None
-    prof = os.path.join(ROOT, "profiles", f"ncu_{args.config}_k{k}.json")
+    prof = os.path.join(ROOT, "profiles", f"ncu_{args.config}_k{k}.json")  # ncu --set full summary
     if os.path.exists(prof):
         with open(prof) as f:
             traffic = json.load(f).get("dram_bytes_per_launch")
@@ -341,6 +341,22 @@ def main():
                 "frac": alu_achieved / alu_peak, "traffic": traffic,
                 "kernel": kernel, "per_launch": f"W(k)={w_k:.1f} reference min/max per sample x "
                 f"{per_launch} samples", "peak_source": "measured (profiles/r01_minmax_microbench.txt)"}
+    # secondary: instruction issue of the dominant kernel -- ncu-measured warp
+    # instructions per sample (committed capture of this config) x the live
+    # sample rate, against 4 warp-instructions/clk/SM x 148 SMs x SM clock
+    roofline_issue = None
+    ncu_prof = os.path.join(ROOT, "profiles", f"ncu_{args.config}_k{k}.json")
+    if os.path.exists(ncu_prof):
+        with open(ncu_prof) as f:
+            npf = json.load(f)
+        ips = npf.get("warp_instructions_per_sample")
+        if ips and kernel in npf.get("kernel", ""):
+            clk_mhz = (clk.summary().get("sm_mhz") or 1965.0)
+            achieved_wi = ips * per_launch / (kern_ms * 1e-3) / 1e12
+            peak_wi = 4 * 148 * clk_mhz * 1e6 / 1e12
+            roofline_issue = {"bound": "issue", "achieved": achieved_wi, "peak": peak_wi,
+                              "unit": "T warp-instr/s", "frac": achieved_wi / peak_wi,
+                              "per_launch": f"{ips} warp instructions per sample (ncu, {ncu_prof[len(ROOT) + 1:]})"}
     roofline_hbm = {"bound": "hbm", "achieved": hbm_achieved, "peak": peaks.get("hbm_gbs"),
                     "unit": "GB/s", "frac": hbm_achieved / peaks.get("hbm_gbs", 6650.0),
                     "traffic": traffic, "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
@@ -355,7 +371,8 @@ def main():
                    "variant": variant, "kernel": kernel, "mode": mode,
                    "l2": "flushed (512 MiB write) before every timed step",
                    "parallelism": f"{mode} x{world}"},
-        "roofline": roofline, "roofline_hbm": roofline_hbm, "e2e": e2e,
+        "roofline": roofline, "roofline_hbm": roofline_hbm, "roofline_issue": roofline_issue,
+        "e2e": e2e,
         "gpu_launches": int(launches), "clocks": clk.summary(),
     }
     if world == 1 and not args.no_cpu_baseline:

@@ -57,6 +57,13 @@ def _compile(src: str) -> tuple[str, str]:
 def build(jobs: int | None = None, force: bool = False, verbose: bool = False) -> str:
     codegen.generate()
     os.makedirs(BUILD, exist_ok=True)
+    # a change of compiler flags (e.g. TMB_NVCC_EXTRA) rebuilds everything
+    stamp = os.path.join(BUILD, "flags.txt")
+    flags = " ".join([NVCC, *ARCH, *FLAGS])
+    if not os.path.exists(stamp) or open(stamp).read() != flags:
+        force = True
+        with open(stamp, "w") as f:
+            f.write(flags)
     newest_hdr = max((os.path.getmtime(h) for h in _headers()), default=0)
     todo = []
     for src in _sources():
