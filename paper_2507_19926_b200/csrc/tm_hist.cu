@@ -48,22 +48,23 @@ namespace {
 
 template <int K, int G>
 struct HistCfg {
-  using S = WarpSweep<K>;
+  using S = WarpSweep<K, 256, 2>;  // 3 columns per lane (10-bit fields) measured slower
+  static constexpr int CPL = S::kCPL;
   static constexpr int H = K / 2;
   static constexpr int RING = K + 2 * G + 1;        // next group lands while this one runs
-  static constexpr int FW = 64 + K - 1;             // footprint columns of the warp
+  static constexpr int FW = S::COLS + K - 1;        // footprint columns of the warp
   static constexpr int RW = ((FW + 3) / 4) * 4 + 8; // ring row bytes (+ slack words)
   static constexpr int kRingBytes = RING * RW;
   static constexpr int kWarpBytes = S::kHistBytes + kRingBytes;
   static constexpr int E = (G * FW + 31) / 32;      // prefetch bytes per lane
 };
 
-// One warp per work item (64 output columns x R rows of one channel); the
+// One warp per work item (32*CPL output columns x R rows of one channel); the
 // warps of a CTA share nothing, so there is no CTA barrier anywhere.
 template <int K, int G, int WPC>
 __global__ void __launch_bounds__(32 * WPC) hist8_kernel(Job job, int R, int n_strips, int n_segs) {
   using C = HistCfg<K, G>;
-  using SW = WarpSweep<K>;
+  using SW = typename C::S;
   extern __shared__ __align__(16) uint32_t smem[];
   const int warp = threadIdx.x >> 5;
   const int tid = threadIdx.x & 31;
@@ -78,7 +79,7 @@ __global__ void __launch_bounds__(32 * WPC) hist8_kernel(Job job, int R, int n_s
     const int chan = item % CH;
     const int strip = (item / CH) % n_strips;
     const int seg = item / (CH * n_strips);
-    const int X0 = strip * 64;
+    const int X0 = strip * SW::COLS;
     const int Y0 = seg * R;
     const int rows = min(R, job.out_h - Y0);
     const uint8_t* src = static_cast<const uint8_t*>(job.src) + chan;
@@ -124,11 +125,12 @@ __global__ void __launch_bounds__(32 * WPC) hist8_kernel(Job job, int R, int n_s
       sw.add_row(ch);
     }
     sw.init_median();
-    const int x = X0 + 2 * tid;
+    const int x = X0 + C::CPL * tid;
     auto store = [&](int yrel) {
       uint8_t* d = dst + (int64_t)(Y0 + yrel) * job.dst_pitch + (int64_t)x * CH;
-      if (x < W) d[0] = (uint8_t)sw.m[0];
-      if (x + 1 < W) d[CH] = (uint8_t)sw.m[1];
+#pragma unroll
+      for (int c = 0; c < C::CPL; c++)
+        if (x + c < W) d[c * CH] = (uint8_t)sw.m[c];
     };
     store(0);
 
@@ -175,7 +177,7 @@ int launch_hist8_k(const Job& job, cudaStream_t stream) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, 32 * WPC, kSmem);
     occ = o > 0 ? o : 1;
   }
-  const int n_strips = (job.width + 63) / 64;
+  const int n_strips = (job.width + C::S::COLS - 1) / C::S::COLS;
   const long slots = (long)sms * occ * WPC;  // concurrent warps
   // Row segment length: long enough to amortise the k x k build (about k rows
   // of work), short enough that the last wave is small -- the candidate with
