@@ -221,8 +221,11 @@ int tm_median2d_host(const void* src, int64_t src_pitch, void* dst, int64_t dst_
   char* din = static_cast<char*>(sc.buf);
   char* dout = din + (size_t)row * height;
   const int halo = k_h / 2;
-  // bands of >= 128 rows, at most kMaxBands
-  const int nb = std::max(1, std::min(kMaxBands, height / 128));
+  // bands of >= 128 rows and >= 2 MB, at most kMaxBands (small images: one
+  // band -- the pipeline only pays once copies dominate the launch overhead)
+  const int64_t img_bytes = row * height;
+  const int nb = (int)std::max<int64_t>(
+      1, std::min<int64_t>({kMaxBands, height / 128, img_bytes / (2 << 20)}));
   int y[kMaxBands + 1];
   for (int b = 0; b <= nb; b++) y[b] = (int)((int64_t)height * b / nb);
   const char* hsrc = static_cast<const char*>(src);
