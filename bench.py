@@ -350,7 +350,9 @@ def main():
         with open(ncu_prof) as f:
             npf = json.load(f)
         ips = npf.get("warp_instructions_per_sample")
-        if ips and kernel in npf.get("kernel", ""):
+        ncu_name = {"oblivious": "obl_kernel", "histogram": "hist8_kernel", "rank": "rank_kernel",
+                    "multipass": "aware", "select": "select"}.get(kernel, kernel)
+        if ips and ncu_name in npf.get("kernel", ""):
             clk_mhz = (clk.summary().get("sm_mhz") or 1965.0)
             achieved_wi = ips * per_launch / (kern_ms * 1e-3) / 1e12
             peak_wi = 4 * 148 * clk_mhz * 1e6 / 1e12
