@@ -47,7 +47,10 @@ struct RankCfg {
   static constexpr int NB = TMB_RANK_FINE_BINS;        // fine key bins
   using SWC = WarpSweep<K, NBC>;
   using SW = WarpSweep<K, NB>;
-  static constexpr int RMAX = 128;
+#ifndef TMB_RANK_BIG_RMAX
+#define TMB_RANK_BIG_RMAX 128
+#endif
+  static constexpr int RMAX = K <= 45 ? 128 : TMB_RANK_BIG_RMAX;
   static constexpr int G = 4;                          // ring refill group (rows)
   static constexpr int H = K / 2;
   static constexpr int FW = 64 + K - 1;                // footprint columns
@@ -56,7 +59,10 @@ struct RankCfg {
   static constexpr int kRingBytes = ((RING * KW + 15) / 16) * 16;
   // candidates per (sub-)item: the median spread of a 64 x 128 item (and so
   // the candidate count) grows with k; small k buys occupancy with less
-  static constexpr int CMAX = K <= 45 ? 2048 : 4096;
+#ifndef TMB_RANK_BIG_CMAX
+#define TMB_RANK_BIG_CMAX 4096
+#endif
+  static constexpr int CMAX = K <= 45 ? 2048 : TMB_RANK_BIG_CMAX;
   static constexpr int kValBytes = CMAX * (int)sizeof(T);
   static constexpr int kPosBytes = CMAX * 2;
   static constexpr int kStartBytes = (NB + 16) * 4;      // start[]
