@@ -4,6 +4,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -181,15 +182,18 @@ int tm_median2d_host(const void* src, int64_t src_pitch, void* dst, int64_t dst_
   if (channels < 1) return fail(TM_EINVAL, "bad channel count %d", channels);
   const int64_t row = (int64_t)width * channels * (bits / 8);
   if (src_pitch < row || dst_pitch < row) return fail(TM_EINVAL, "pitch smaller than a row");
-  // Row bands pipelined over three streams: band b's H2D copy, band b-1's
-  // filter and band b-2's D2H copy run concurrently (PCIe is full duplex), so
-  // the call costs about max(H2D, filter, D2H) instead of their sum.  A band's
+  // Row bands pipelined over streams: band b's H2D copy, the filters of
+  // earlier bands (three filter streams, so band kernels overlap each other's
+  // tails) and their D2H copies run concurrently (PCIe is full duplex), so the
+  // call costs about max(H2D, filter, D2H) instead of their sum.  A band's
   // filter waits for the input chunk holding its last halo row.
-  constexpr int kMaxBands = 16;
+  constexpr int kMaxBands = 32;
+  constexpr int kFilterStreams = 3;  // band kernels overlap each other's tails
   struct Scratch {
     void* buf = nullptr;
     size_t bytes = 0;
     cudaStream_t st[3] = {nullptr, nullptr, nullptr};  // h2d, filter, d2h
+    cudaStream_t fs[kFilterStreams] = {};               // concurrent band filters
     cudaEvent_t ev_in[kMaxBands] = {}, ev_out[kMaxBands] = {};
   };
   static thread_local std::vector<Scratch> per_dev;
@@ -212,6 +216,10 @@ int tm_median2d_host(const void* src, int64_t src_pitch, void* dst, int64_t dst_
       e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
       if (e != cudaSuccess) return fail(TM_ECUDA, "cudaStreamCreate: %s", cudaGetErrorString(e));
     }
+    for (auto& st : sc.fs) {
+      e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+      if (e != cudaSuccess) return fail(TM_ECUDA, "cudaStreamCreate: %s", cudaGetErrorString(e));
+    }
     for (int b = 0; b < kMaxBands; b++) {
       e = cudaEventCreateWithFlags(&sc.ev_in[b], cudaEventDisableTiming);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&sc.ev_out[b], cudaEventDisableTiming);
@@ -221,43 +229,55 @@ int tm_median2d_host(const void* src, int64_t src_pitch, void* dst, int64_t dst_
   char* din = static_cast<char*>(sc.buf);
   char* dout = din + (size_t)row * height;
   const int halo = k_h / 2;
-  // bands of >= 128 rows and >= 2 MB, at most kMaxBands (small images: one
-  // band -- the pipeline only pays once copies dominate the launch overhead)
+  // bands of >= 64 rows and >= 2 MB, at most 16 (measured on C2: 1 -> 19.3,
+  // 4 -> 27.8, 8 -> 34.7, 16 -> 38.7, 32 -> 35.5 Gpixel/s e2e); small images
+  // get one band -- the pipeline only pays once copies dominate
   const int64_t img_bytes = row * height;
-  const int nb = (int)std::max<int64_t>(
-      1, std::min<int64_t>({kMaxBands, height / 128, img_bytes / (2 << 20)}));
+  static const int force_nb = [] {  // experiments: TMB_HOST_BANDS
+    const char* v = getenv("TMB_HOST_BANDS");
+    return v ? atoi(v) : 0;
+  }();
+  const int nb = force_nb > 0 ? std::min(std::min(force_nb, kMaxBands), height)
+                              : (int)std::max<int64_t>(1, std::min<int64_t>(
+                                    {16, height / 64, img_bytes / (2 << 20)}));
   int y[kMaxBands + 1];
   for (int b = 0; b <= nb; b++) y[b] = (int)((int64_t)height * b / nb);
   const char* hsrc = static_cast<const char*>(src);
   char* hdst = static_cast<char*>(dst);
   for (int b = 0; b < nb; b++) {
-    e = cudaMemcpy2DAsync(din + (size_t)y[b] * row, row, hsrc + (int64_t)y[b] * src_pitch,
-                          src_pitch, row, y[b + 1] - y[b], cudaMemcpyHostToDevice, sc.st[0]);
+    const size_t n_rows = (size_t)(y[b + 1] - y[b]);
+    e = src_pitch == row
+            ? cudaMemcpyAsync(din + (size_t)y[b] * row, hsrc + (int64_t)y[b] * src_pitch,
+                              n_rows * row, cudaMemcpyHostToDevice, sc.st[0])
+            : cudaMemcpy2DAsync(din + (size_t)y[b] * row, row, hsrc + (int64_t)y[b] * src_pitch,
+                                src_pitch, row, n_rows, cudaMemcpyHostToDevice, sc.st[0]);
     if (e == cudaSuccess) e = cudaEventRecord(sc.ev_in[b], sc.st[0]);
     if (e != cudaSuccess) return fail(TM_ECUDA, "H2D copy: %s", cudaGetErrorString(e));
   }
-  int have = -1;  // newest input chunk the filter stream already waits for
   for (int b = 0; b < nb; b++) {
+    cudaStream_t fst = sc.fs[b % kFilterStreams];
     const int last_src = std::min(height, y[b + 1] + halo) - 1;
     int chunk = b;
     while (chunk + 1 < nb && y[chunk + 1] <= last_src) chunk++;
-    if (chunk > have) {
-      e = cudaStreamWaitEvent(sc.st[1], sc.ev_in[chunk], 0);
-      if (e != cudaSuccess) return fail(TM_ECUDA, "stream wait: %s", cudaGetErrorString(e));
-      have = chunk;
-    }
+    e = cudaStreamWaitEvent(fst, sc.ev_in[chunk], 0);
+    if (e != cudaSuccess) return fail(TM_ECUDA, "stream wait: %s", cudaGetErrorString(e));
     rc = tm_median2d_band(din, row, height, y[b], y[b + 1] - y[b], dout + (size_t)y[b] * row, row,
-                          width, channels, bits, k_w, k_h, variant, sc.st[1]);
+                          width, channels, bits, k_w, k_h, variant, fst);
     if (rc) return rc;
-    e = cudaEventRecord(sc.ev_out[b], sc.st[1]);
+    e = cudaEventRecord(sc.ev_out[b], fst);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(sc.st[2], sc.ev_out[b], 0);
     if (e == cudaSuccess)
-      e = cudaMemcpy2DAsync(hdst + (int64_t)y[b] * dst_pitch, dst_pitch, dout + (size_t)y[b] * row,
-                            row, row, y[b + 1] - y[b], cudaMemcpyDeviceToHost, sc.st[2]);
+      e = dst_pitch == row
+              ? cudaMemcpyAsync(hdst + (int64_t)y[b] * dst_pitch, dout + (size_t)y[b] * row,
+                                (size_t)(y[b + 1] - y[b]) * row, cudaMemcpyDeviceToHost, sc.st[2])
+              : cudaMemcpy2DAsync(hdst + (int64_t)y[b] * dst_pitch, dst_pitch,
+                                  dout + (size_t)y[b] * row, row, row, y[b + 1] - y[b],
+                                  cudaMemcpyDeviceToHost, sc.st[2]);
     if (e != cudaSuccess) return fail(TM_ECUDA, "D2H copy: %s", cudaGetErrorString(e));
   }
   e = cudaStreamSynchronize(sc.st[2]);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(sc.st[1]);
+  for (auto& st : sc.fs)
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(sc.st[0]);
   if (e != cudaSuccess) return fail(TM_ECUDA, "kernel failed: %s", cudaGetErrorString(e));
   return TM_OK;
