@@ -182,18 +182,20 @@ int launch_hist8_k(const Job& job, cudaStream_t stream) {
   // Row segment length: long enough to amortise the k x k build (about k rows
   // of work), short enough that the last wave is small -- the candidate with
   // the smallest estimated makespan.
+  // every segment count (R = ceil(out_h / segs)), so the item count can land
+  // just under a multiple of the resident warps
   int best_R = job.out_h;
   long best_cost = 0x7fffffffffffL;
-  for (int R = 16; R <= 16384; R *= 2) {
-    const long segs = (job.out_h + R - 1) / R;
-    const long items = segs * n_strips * job.channels;
+  for (int segs = 1; segs <= (job.out_h + 15) / 16; segs++) {
+    const int R = (job.out_h + segs - 1) / segs;
+    if (segs > 1 && R == (job.out_h + segs - 2) / (segs - 1)) continue;  // same R as segs - 1
+    const long items = (long)segs * n_strips * job.channels;
     const long waves = (items + slots - 1) / slots;
-    const long cost = waves * (long)(min(R, job.out_h) + K + 8);
+    const long cost = waves * (long)(R + K + 8);
     if (cost < best_cost) {
       best_cost = cost;
       best_R = R;
     }
-    if (R >= job.out_h) break;
   }
   const int R = best_R;
   const int n_segs = (job.out_h + R - 1) / R;

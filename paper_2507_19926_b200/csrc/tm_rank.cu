@@ -484,18 +484,20 @@ int launch_rank_k(const Job& job, cudaStream_t stream) {
   }
   const int n_strips = (job.width + 63) / 64;
   const long slots = (long)sms * occ;
+  // every segment count with R = ceil(out_h / segs) <= RMAX, so the item
+  // count can land just under a multiple of the resident warps
   int best_R = C::RMAX;
   long best_cost = 0x7fffffffffffL;
-  for (int R = 8; R <= C::RMAX; R *= 2) {
-    const long segs = (job.out_h + R - 1) / R;
-    const long items = segs * n_strips * job.channels;
+  for (int segs = (job.out_h + C::RMAX - 1) / C::RMAX; segs <= (job.out_h + 7) / 8; segs++) {
+    const int R = (job.out_h + segs - 1) / segs;
+    const long items = (long)segs * n_strips * job.channels;
     const long waves = (items + slots - 1) / slots;
-    const long cost = waves * (long)(min(R, job.out_h) + K + 8);
+    // two sweeps of (rows + ~K build) each
+    const long cost = waves * (long)(R + K + 8);
     if (cost < best_cost) {
       best_cost = cost;
       best_R = R;
     }
-    if (R >= job.out_h) break;
   }
   const int R = best_R;
   const int n_segs = (job.out_h + R - 1) / R;
