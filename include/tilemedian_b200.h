@@ -50,7 +50,8 @@ enum {
   TM_KERNEL_MULTIPASS = 2, /* the reference's multi-pass aware engine on the GPU (aware.py:437-492) */
   TM_KERNEL_SELECT = 3,    /* brute-force per-pixel radix selection ("oracle") */
   TM_KERNEL_HISTOGRAM = 4, /* 8-bit sliding column histograms: variant (2) for uint8 */
-  TM_KERNEL_RANK = 5       /* 16/32-bit coarse + candidate-key histogram sweeps: variant (2) */
+  TM_KERNEL_RANK = 5,      /* 16/32-bit coarse + candidate-key histogram sweeps: variant (2) */
+  TM_KERNEL_MED3 = 6       /* k = 3: register sliding window, shared column sorts: variant (1) */
 };
 
 enum { TM_OK = 0, TM_EINVAL = 1, TM_ETYPE = 2, TM_ECUDA = 3 };

@@ -46,6 +46,7 @@ bool supports(int kernel, int bits, int kw, int kh) {
     case TM_KERNEL_SELECT: return true;
     case TM_KERNEL_HISTOGRAM: return square && bits == 8 && tmb::hist8_supports(kw);
     case TM_KERNEL_RANK: return square && tmb::rank_supports(bits, kw);
+    case TM_KERNEL_MED3: return square && kw == 3;
     default: return false;
   }
 }
@@ -63,6 +64,7 @@ int aware_kernel(int bits, int k) {
 // .jsonl): the oblivious network up to the crossover, the data-aware kernel
 // from it on.  Crossovers: 8-bit k = 15, 16-bit k = 29, 32-bit k = 27.
 int auto_kernel(int bits, int k) {
+  if (k == 3) return TM_KERNEL_MED3;
   const int crossover = bits == 8 ? 15 : (bits == 16 ? 29 : 27);
   if (k < crossover && find_obl(bits, k)) return TM_KERNEL_OBLIVIOUS;
   return aware_kernel(bits, k);
@@ -75,6 +77,7 @@ int route(int bits, int kw, int kh, int variant) {
     case TM_VARIANT_ORACLE:
       return TM_KERNEL_SELECT;
     case TM_VARIANT_OBLIVIOUS:
+      if (square && kw == 3) return TM_KERNEL_MED3;  // the k = 3 network, specialised
       return (square && find_obl(bits, kw)) ? TM_KERNEL_OBLIVIOUS : TM_KERNEL_SELECT;
     case TM_VARIANT_AWARE:
       return (square && kw >= 9) ? aware_kernel(bits, kw) : TM_KERNEL_SELECT;
@@ -142,6 +145,9 @@ int tm_median2d_band(const void* src, int64_t src_pitch, int32_t src_rows, int32
       break;
     case TM_KERNEL_RANK:
       err = tmb::launch_rank(bits, job, k_w, s);
+      break;
+    case TM_KERNEL_MED3:
+      err = tmb::launch_med3(bits, job, s);
       break;
     default:
       err = tmb::launch_select(bits, job, k_w, k_h, s);
@@ -295,6 +301,7 @@ const char* tm_kernel_name(int32_t kernel) {
     case TM_KERNEL_SELECT: return "select";
     case TM_KERNEL_HISTOGRAM: return "histogram";
     case TM_KERNEL_RANK: return "rank";
+    case TM_KERNEL_MED3: return "med3";
     default: return "none";
   }
 }

@@ -20,5 +20,6 @@ bool hist8_supports(int k);
 int launch_hist8(const Job& job, int k, cudaStream_t s);
 bool rank_supports(int bits, int k);
 int launch_rank(int bits, const Job& job, int k, cudaStream_t s);
+int launch_med3(int bits, const Job& job, cudaStream_t s);
 
 }  // namespace tmb

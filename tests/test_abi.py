@@ -37,7 +37,8 @@ def test_version_and_kernel_names():
 
 def test_dispatch_query_routes():
     lib = _lib.load()
-    assert lib.tm_dispatch_query(8, 3, 3, 0) == 1          # auto, small k -> oblivious kernel
+    assert lib.tm_dispatch_query(8, 5, 5, 0) == 1          # auto, small k -> oblivious kernel
+    assert lib.tm_dispatch_query(8, 3, 3, 0) == 6          # k = 3 -> specialised network
     assert lib.tm_dispatch_query(16, 9, 9, 3) == 3         # oracle -> brute-force select
     assert lib.tm_dispatch_query(8, 3, 5, 1) in (1, 2, 3)  # rectangular
     assert lib.tm_dispatch_query(12, 3, 3, 0) == 0         # bad width

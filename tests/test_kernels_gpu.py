@@ -139,3 +139,39 @@ def test_multipass_kernel(bits):
     for name, img in images(bits, 97, 131, seed=bits):
         for k in (9, 25):
             assert np.array_equal(run_forced("multipass", img, k), oracle_median_filter_c(img, k)), (name, k)
+
+
+@pytest.mark.parametrize("bits", [8, 16, 32])
+def test_med3_patterns_and_shapes(bits):
+    for name, img in images(bits, 157, 301, seed=3):
+        assert np.array_equal(run_forced("med3", img, 3), oracle_median_filter_c(img, 3)), name
+    dt = {8: np.uint8, 16: np.uint16, 32: np.uint32}[bits]
+    rng = np.random.default_rng(bits)
+    for shape in [(1, 1), (1, 9), (9, 1), (2, 2), (3, 17), (70, 1031), (513, 64), (5, 8)]:
+        img = rng.integers(0, np.iinfo(dt).max, size=shape, dtype=dt, endpoint=True)
+        assert np.array_equal(run_forced("med3", img, 3), oracle_median_filter_c(img, 3)), shape
+
+
+def test_med3_interleaved_and_band():
+    rng = np.random.default_rng(33)
+    img = rng.integers(0, 256, (90, 77, 3), dtype=np.uint8)
+    out = run_forced("med3", img, 3)
+    for c in range(3):
+        assert np.array_equal(out[..., c], oracle_median_filter_c(np.ascontiguousarray(img[..., c]), 3))
+    # band entry point: output rows of a source with halo rows
+    lib = _lib.load()
+    full = rng.integers(0, 65536, (200, 256), dtype=np.uint16)
+    ref = oracle_median_filter_c(full, 3)
+    dev = torch.from_numpy(full.astype(np.int32)).to(torch.uint16).cuda()
+    prev = lib.tm_force_kernel(_lib.KERNEL_CODES["med3"])
+    try:
+        for y0, y1 in ((0, 37), (37, 38), (38, 150), (150, 200)):
+            s0, s1 = max(0, y0 - 1), min(200, y1 + 1)
+            src = dev[s0:s1].contiguous()
+            dst = torch.empty((y1 - y0, 256), dtype=torch.uint16, device="cuda")
+            _lib.check(lib.tm_median2d_band(src.data_ptr(), 512, s1 - s0, y0 - s0, y1 - y0,
+                                            dst.data_ptr(), 512, 256, 1, 16, 3, 3, 0, None))
+            torch.cuda.synchronize()
+            assert np.array_equal(dst.cpu().numpy().astype(np.uint16), ref[y0:y1]), (y0, y1)
+    finally:
+        lib.tm_force_kernel(prev)
