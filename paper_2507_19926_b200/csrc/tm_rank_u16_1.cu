@@ -1,0 +1,31 @@
+// tm_rank_u16_1.cu -- instantiations of the rank kernel (tm_rank.cuh) for
+// u16 and k in {5, 13, 21, 29, 37, 45, 53, 61, 69} (split so the build compiles in parallel).
+#include "tm_rank.cuh"
+
+namespace tmb {
+
+int launch_rank_u16_1(int k, const Job& job, cudaStream_t s) {
+  switch (k) {
+    case 5: return launch_rank_k<uint16_t, 5>(job, s);
+    case 13: return launch_rank_k<uint16_t, 13>(job, s);
+    case 21: return launch_rank_k<uint16_t, 21>(job, s);
+    case 29: return launch_rank_k<uint16_t, 29>(job, s);
+    case 37: return launch_rank_k<uint16_t, 37>(job, s);
+    case 45: return launch_rank_k<uint16_t, 45>(job, s);
+    case 53: return launch_rank_k<uint16_t, 53>(job, s);
+    case 61: return launch_rank_k<uint16_t, 61>(job, s);
+    case 69: return launch_rank_k<uint16_t, 69>(job, s);
+    default: return (int)cudaErrorInvalidValue;
+  }
+}
+
+#ifdef TMB_RANK_PROFILE
+void rank_prof_take_u16_1(unsigned long long* acc) {
+  unsigned long long v[8], z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  cudaMemcpyFromSymbol(v, g_rank_prof, sizeof(v));
+  cudaMemcpyToSymbol(g_rank_prof, z, sizeof(z));
+  for (int i = 0; i < 8; i++) acc[i] += v[i];
+}
+#endif
+
+}  // namespace tmb
