@@ -127,8 +127,7 @@ static __device__ unsigned long long g_rank_prof[8];  // per translation unit; t
 #endif
 
 template <typename T, int K>
-__global__ void __launch_bounds__(32) rank_kernel(Job job, int R, int n_strips, int n_segs,
-                                                  int margin8) {
+__global__ void __launch_bounds__(32) rank_kernel(Job job, int R, int n_strips, int n_segs) {
   using C = RankCfg<T, K>;
   using SW = typename C::SW;
   extern __shared__ __align__(16) uint32_t smem[];
@@ -143,13 +142,6 @@ __global__ void __launch_bounds__(32) rank_kernel(Job job, int R, int n_strips, 
   sw.init(smem, lane);
   const int W = job.width, SH = job.src_h, CH = job.channels;
   const int n_items = n_strips * CH * n_segs;
-  constexpr uint32_t kTMax = (uint32_t)(((uint64_t)1 << C::BITS) - 1);
-
-  // Speculative candidate range: the previous (sub-)item's median range of
-  // this warp, widened; a pixel whose median falls outside makes the
-  // sub-item redo with the exact coarse pass.
-  bool spec = false;
-  uint32_t spec_lo = 0, spec_hi = 0;
 
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
     const int chan = item % CH;
@@ -163,7 +155,6 @@ __global__ void __launch_bounds__(32) rank_kernel(Job job, int R, int n_strips, 
     const int x = X0 + 2 * lane;
 
     int Rcur = rows_item;
-    bool exact = !spec;
     for (int y0 = 0; y0 < rows_item;) {
       const int rows = min(Rcur, rows_item - y0);
       const int Y0 = Yi + y0;
@@ -247,9 +238,9 @@ __global__ void __launch_bounds__(32) rank_kernel(Job job, int R, int n_strips, 
 #ifdef TMB_RANK_PROFILE
       long long _t = clock64();
 #endif
-      // ---- 1. candidate range: exact coarse pass, or speculative ----------
+      // ---- 1. candidate range: the exact coarse pass ------------------------
       uint32_t lo, hi;
-      if (exact) {
+      {
         int blo = C::NBC - 1, bhi = 0;
         KeyFn<C::NBC> kc{0u, 0u, 0u, -1, C::SHIFT};
         sweep(swc, kc, [&](int) {
@@ -268,9 +259,6 @@ __global__ void __launch_bounds__(32) rank_kernel(Job job, int R, int n_strips, 
         }
         lo = (uint32_t)blo << C::SHIFT;
         hi = (uint32_t)(((uint64_t)(bhi + 1) << C::SHIFT) - 1);
-      } else {
-        lo = spec_lo;
-        hi = spec_hi;
       }
       // value -> fine bin: identity when [lo, hi] has at most NB - 2 values,
       // else floor((v - lo) * (NB - 2) / (hi - lo + 1)) via a 32.32 multiplier
@@ -330,10 +318,6 @@ __global__ void __launch_bounds__(32) rank_kernel(Job job, int R, int n_strips, 
         }
         __syncwarp();
         if (n_cand > C::CMAX) {
-          if (!exact) {  // the speculative range was too wide: get the exact one
-            exact = true;
-            continue;
-          }
           if (rows > 1) {  // too many candidates: halve the sub-item
             Rcur = (rows + 1) / 2;
             continue;
@@ -344,8 +328,6 @@ __global__ void __launch_bounds__(32) rank_kernel(Job job, int R, int n_strips, 
                   (T)brute_median<T, K>(src, job, job.out_y0 + Y0, x + c);
           y0 += rows;
           Rcur = rows_item;
-          spec = false;
-          exact = true;
           continue;
         }
         RANK_T(1);
@@ -396,16 +378,13 @@ __global__ void __launch_bounds__(32) rank_kernel(Job job, int R, int n_strips, 
 
       RANK_T(3);
       // ---- 3. fine pass -----------------------------------------------------
-      bool miss = false;
-      uint32_t mlo = kTMax, mhi = 0;
       sweep(sw, kf, [&](int t) {
 #pragma unroll
         for (int c = 0; c < 2; c++) {
           const int b = sw.m[c];
           uint32_t v = 0;
           if (b < 1 || b > C::NB - 2) {
-            // outside [lo, hi]: a speculative miss (or a column beyond the edge)
-            miss |= x + c < W;
+            // only columns beyond the image edge (excluded from [lo, hi]) land here
           } else if (f == 0) {
             v = lo + (uint32_t)(b - 1);
           } else {
@@ -435,30 +414,10 @@ __global__ void __launch_bounds__(32) rank_kernel(Job job, int R, int n_strips, 
             for (; need > 0 && i < i1; i++)
               if (inwin(cpos[i]) && --need == 0) v = cval[i];
           }
-          if (x + c < W) {
-            mlo = min(mlo, v);
-            mhi = max(mhi, v);
-            dst[(int64_t)(Y0 + t) * job.dst_pitch + (int64_t)(x + c) * CH] = (T)v;
-          }
+          if (x + c < W) dst[(int64_t)(Y0 + t) * job.dst_pitch + (int64_t)(x + c) * CH] = (T)v;
         }
       });
       RANK_T(4);
-      if (__any_sync(0xffffffffu, miss)) {  // speculation failed: redo exactly
-        exact = true;
-        continue;
-      }
-      for (int o = 16; o; o >>= 1) {
-        mlo = min(mlo, __shfl_xor_sync(0xffffffffu, mlo, o));
-        mhi = max(mhi, __shfl_xor_sync(0xffffffffu, mhi, o));
-      }
-      if (margin8 > 0 && mlo <= mhi) {
-        const uint32_t w = mhi - mlo;
-        const uint32_t mg = (uint32_t)(((uint64_t)w * (uint32_t)margin8) / 8u) + 1u;
-        spec_lo = mlo > mg ? mlo - mg : 0u;
-        spec_hi = kTMax - mhi > mg ? mhi + mg : kTMax;
-        spec = true;
-      }
-      exact = !spec;
       y0 += rows;
       Rcur = rows_item;
     }
@@ -504,13 +463,7 @@ int launch_rank_k(const Job& job, cudaStream_t stream) {
   const int n_segs = (job.out_h + R - 1) / R;
   const long items = (long)n_segs * n_strips * job.channels;
   const int grid = (int)(items < slots ? items : slots);
-  static const int margin8 = [] {
-    // speculative candidate range (margin in 1/8 of the previous item's median
-    // range); off by default -- measured slower on B200 (profiles/)
-    const char* v = getenv("TMB_RANK_MARGIN8");
-    return v ? atoi(v) : 0;
-  }();
-  fn<<<grid, 32, kSmem, stream>>>(job, R, n_strips, n_segs, margin8);
+  fn<<<grid, 32, kSmem, stream>>>(job, R, n_strips, n_segs);
   return (int)cudaGetLastError();
 }
 

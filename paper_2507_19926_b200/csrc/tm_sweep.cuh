@@ -47,10 +47,7 @@ __device__ __forceinline__ void st_hist(uint32_t a, uint32_t v) {
 }
 
 // CPL = output columns per lane sharing one count word: 2 (u16 fields, any K)
-// or 3 (10-bit fields, K^2 <= 1023 i.e. K <= 31).
-template <int K>
-constexpr int default_cpl() { return K * K <= 1023 ? 3 : 2; }
-
+// or 3 (10-bit fields, K^2 <= 1023 i.e. K <= 31; measured slower).
 template <int K, int NB = 256, int CPL = 2>
 struct WarpSweep {
   static_assert(CPL == 2 || (CPL == 3 && K * K <= 1023), "counts must fit their fields");
