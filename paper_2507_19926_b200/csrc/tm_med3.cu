@@ -197,11 +197,13 @@ int launch_med3_t(const Job& job, cudaStream_t stream) {
   }
   const int n_tx = (job.width + TX - 1) / TX;
   // rows per strip: enough threads for ~4 full waves of 2048 threads/SM, at
-  // least 4 rows (the 2 halo rows per strip are re-read)
+  // least 1 row (small images: parallelism over the 2 re-read halo rows)
   const long pair_rows = (job.out_h + L - 1) / L;
   const long want_threads = (long)sms * 2048 * 4;
   long R = (long)n_tx * job.channels * pair_rows / want_threads;
-  R = R < 4 ? 4 : (R > 64 ? 64 : R);
+  R = R < 1 ? 1 : (R > 64 ? 64 : R);
+  // short strips only when 4-row strips would fill less than a quarter wave
+  if (R < 4 && 4 * (long)n_tx * job.channels * ((pair_rows + 3) / 4) >= (long)sms * 2048) R = 4;
   if (R > pair_rows) R = pair_rows;
   const uintptr_t base_s = reinterpret_cast<uintptr_t>(job.src);
   const uintptr_t base_d = reinterpret_cast<uintptr_t>(job.dst);
