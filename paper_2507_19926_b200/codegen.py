@@ -53,8 +53,8 @@ OBLIVIOUS_CONFIGS = {
     9: OblConfig(9, 4, 2, 32, 4),
     11: OblConfig(11, 4, 2, 32, 4),
     13: OblConfig(13, 4, 4, 32, 4),
-    15: OblConfig(15, 4, 4, 32, 4),
-    # k >= 17: a 4x4 root tile's live state exceeds the register file of one
+    15: OblConfig(15, 4, 4, 32, 4, pair=True),  # pair: +32 % over one thread per tile
+    # k >= 15: a 4x4 root tile's live state exceeds the register file of one
     # thread -- split each tile over a thread pair (pairgen.py)
     17: OblConfig(17, 4, 4, 32, 4, pair=True),
     19: OblConfig(19, 4, 4, 32, 4, pair=True),
