@@ -51,8 +51,8 @@ OBLIVIOUS_CONFIGS = {
     5: OblConfig(5, 4, 4, 32, 4),  # 4x4: +5 % over 4x2 (round-1 config search)
     7: OblConfig(7, 4, 4, 32, 4),  # 4x4: +2 %
     9: OblConfig(9, 4, 2, 32, 4),
-    11: OblConfig(11, 4, 4, 32, 4),  # 4x4: +7 %; k = 9 stays 4x2 (4x4: -11 %)
-    13: OblConfig(13, 4, 4, 32, 4),
+    11: OblConfig(11, 4, 4, 64, 4),  # 4x4: +7 %, 64-wide CTA +7 %; k = 9 stays 4x2 (4x4: -11 %)
+    13: OblConfig(13, 4, 4, 64, 4),  # 64-wide CTA: +9 %
     15: OblConfig(15, 4, 4, 32, 4, pair=True),  # pair: +32 % over one thread per tile
     # k >= 15: a 4x4 root tile's live state exceeds the register file of one
     # thread -- split each tile over a thread pair (pairgen.py)
