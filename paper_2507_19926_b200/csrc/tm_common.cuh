@@ -126,4 +126,25 @@ __device__ __forceinline__ void store_row(const Job& job, int y, int x0, const T
     if (x0 + i < job.width) store_px<T>(job, y, x0 + i, v[i]);
 }
 
+// Per-kernel launch facts, computed once (C++11 thread-safe static init at
+// the call site): opt-in shared-memory limit, SM count, resident CTAs per SM.
+struct LaunchInfo {
+  cudaError_t err;
+  int sms;
+  int occ;
+};
+template <typename F>
+inline LaunchInfo launch_info(F fn, int threads, int smem) {
+  LaunchInfo li{cudaSuccess, 0, 1};
+  li.err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (li.err != cudaSuccess) return li;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&li.sms, cudaDevAttrMultiProcessorCount, dev);
+  int o = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, threads, smem);
+  li.occ = o > 0 ? o : 1;
+  return li;
+}
+
 }  // namespace tmb

@@ -165,18 +165,9 @@ int launch_hist8_k(const Job& job, cudaStream_t stream) {
   constexpr int kSmem = C::kWarpBytes * WPC;
   static_assert(kSmem <= 227 * 1024, "histogram kernel does not fit in shared memory");
   auto fn = hist8_kernel<K, G, WPC>;
-  static int occ = -1;
-  static int sms = 0;
-  if (occ < 0) {
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-    if (e != cudaSuccess) return (int)e;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    int o = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, 32 * WPC, kSmem);
-    occ = o > 0 ? o : 1;
-  }
+  static const LaunchInfo li = launch_info(fn, 32 * WPC, kSmem);
+  if (li.err != cudaSuccess) return (int)li.err;
+  const int sms = li.sms, occ = li.occ;
   const int n_strips = (job.width + C::S::COLS - 1) / C::S::COLS;
   const long slots = (long)sms * occ * WPC;  // concurrent warps
   // Row segment length: long enough to amortise the k x k build (about k rows

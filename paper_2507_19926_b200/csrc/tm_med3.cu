@@ -189,12 +189,12 @@ __global__ void __launch_bounds__(NT) med3_kernel(Job job, int R, int n_tx, int 
 template <typename T>
 int launch_med3_t(const Job& job, cudaStream_t stream) {
   constexpr int L = M3<T>::L;
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
+  static const int sms = [] {
+    int dev = 0, n = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 148;
+  }();
   const int n_tx = (job.width + TX - 1) / TX;
   // rows per strip: enough threads for ~4 full waves of 2048 threads/SM, at
   // least 1 row (small images: parallelism over the 2 re-read halo rows)

@@ -430,18 +430,9 @@ int launch_rank_k(const Job& job, cudaStream_t stream) {
   constexpr int kSmem = C::kWarpBytes;
   static_assert(kSmem <= 227 * 1024, "rank kernel does not fit in shared memory");
   auto fn = rank_kernel<T, K>;
-  static int occ = -1;
-  static int sms = 0;
-  if (occ < 0) {
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-    if (e != cudaSuccess) return (int)e;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    int o = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, 32, kSmem);
-    occ = o > 0 ? o : 1;
-  }
+  static const LaunchInfo li = launch_info(fn, 32, kSmem);
+  if (li.err != cudaSuccess) return (int)li.err;
+  const int sms = li.sms, occ = li.occ;
   const int n_strips = (job.width + 63) / 64;
   const long slots = (long)sms * occ;
   // every segment count with R = ceil(out_h / segs) <= RMAX, so the item
