@@ -156,7 +156,15 @@ __global__ void __launch_bounds__(32 * WPC) hist8_kernel(Job job, int R, int n_s
 // Warps per CTA: 1 (CTAs are independent anyway; the hardware packs as many
 // as shared memory allows onto each SM).
 template <int K>
-constexpr int hist_g() { return K <= 31 ? 8 : 4; }
+constexpr int hist_g() {
+#ifdef TMB_HIST_G
+  return TMB_HIST_G;
+#else
+  // ring refill group: measured per k range (k = 25: G 8 -> 2 is +18 %;
+  // k <= 17 and k >= 33 prefer 8 and 4)
+  return K <= 21 ? 8 : (K <= 31 ? 2 : 4);
+#endif
+}
 
 template <int K>
 int launch_hist8_k(const Job& job, cudaStream_t stream) {
