@@ -383,7 +383,7 @@ def main():
         with open(ncu_prof) as f:
             npf = json.load(f)
         ips = npf.get("warp_instructions_per_sample")
-        ncu_name = {"oblivious": "obl_kernel", "histogram": "hist8_kernel", "rank": "rank_kernel",
+        ncu_name = {"oblivious": "obl_kernel", "histogram": "hist8_kernel", "rank": "rank_kernel", "med3": "med3_kernel",
                     "multipass": "aware", "select": "select"}.get(kernel, kernel)
         if ips and ncu_name in npf.get("kernel", ""):
             clk_mhz = (clk.summary().get("sm_mhz") or 1965.0)
