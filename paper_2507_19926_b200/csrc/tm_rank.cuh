@@ -66,7 +66,8 @@ struct RankCfg {
 #ifndef TMB_RANK_BIG_CMAX
 #define TMB_RANK_BIG_CMAX 4096
 #endif
-  static constexpr int CMAX = K <= 45 ? 2048 : TMB_RANK_BIG_CMAX;
+  static constexpr int CMAX =
+      K <= 45 ? 2048 : (sizeof(T) == 2 && K <= 53 ? 3072 : TMB_RANK_BIG_CMAX);  // measured
   static constexpr int kValBytes = CMAX * (int)sizeof(T);
   static constexpr int kPosBytes = CMAX * 2;
   static constexpr int kStartBytes = (NB + 16) * 4;      // start[]
