@@ -160,9 +160,9 @@ constexpr int hist_g() {
 #ifdef TMB_HIST_G
   return TMB_HIST_G;
 #else
-  // ring refill group: measured per k range (k = 25: G 8 -> 2 is +18 %;
-  // k <= 17 and k >= 33 prefer 8 and 4)
-  return K <= 21 ? 8 : (K <= 31 ? 2 : 4);
+  // ring refill group: measured per k range (k = 19, 21: G 8 -> 4 is +14 %;
+  // k = 25: G 8 -> 2 is +18 %; k <= 17 prefers 8, k >= 33 prefers 4)
+  return K <= 17 ? 8 : (K <= 21 ? 4 : (K <= 31 ? 2 : 4));
 #endif
 }
 
