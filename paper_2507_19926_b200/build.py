@@ -47,11 +47,22 @@ def _obj(src: str) -> str:
 
 def _compile(src: str) -> tuple[str, str]:
     obj = _obj(src)
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+    cmd = [NVCC, *ARCH, *FLAGS, "-MD", "-MF", obj[:-2] + ".d", "-c", src, "-o", obj]
     p = subprocess.run(cmd, capture_output=True, text=True)
     if p.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{p.stderr[-6000:]}")
     return src, p.stderr
+
+
+def _deps(obj: str) -> list[str] | None:
+    """Headers `obj` was compiled against (nvcc -MD), None when unknown."""
+    try:
+        text = open(obj[:-2] + ".d").read()
+    except OSError:
+        return None
+    text = text.replace("\\\n", " ")
+    _, _, rest = text.partition(":")
+    return [d for d in rest.split() if d]
 
 
 def build(jobs: int | None = None, force: bool = False, verbose: bool = False) -> str:
@@ -68,8 +79,16 @@ def build(jobs: int | None = None, force: bool = False, verbose: bool = False) -
     todo = []
     for src in _sources():
         obj = _obj(src)
-        if (force or not os.path.exists(obj) or os.path.getmtime(obj) < os.path.getmtime(src)
-                or os.path.getmtime(obj) < newest_hdr):
+        if force or not os.path.exists(obj) or os.path.getmtime(obj) < os.path.getmtime(src):
+            todo.append(src)
+            continue
+        deps = _deps(obj)
+        t_obj = os.path.getmtime(obj)
+        if deps is None:
+            stale = t_obj < newest_hdr
+        else:
+            stale = any(not os.path.exists(d) or os.path.getmtime(d) > t_obj for d in deps)
+        if stale:
             todo.append(src)
     logs = {}
     if todo:
