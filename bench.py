@@ -35,6 +35,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -146,27 +147,67 @@ class ClockSampler:
                 "source": self.source}
 
 
-def cpu_baseline(cfg, k, seconds=10.0, threads=None):
-    """The C oracle port on a crop sized for ~`seconds` of host work."""
-    from oracle import load_c_oracle  # test infrastructure: reported baseline only
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor() or "unknown"
+
+
+def cpu_baseline(cfg, k, seconds=10.0, threads=None, src=None, ours=None):
+    """The C oracle port (the reference algorithm, reference.py:26-43) on a
+    crop of the workload sized for ~`seconds` of host work, all host threads.
+
+    With ``src`` / ``ours`` (the bench's device input and GPU output) the crop
+    is cut from the real input -- rows around the image middle, columns from
+    the left edge -- and the oracle's result is compared with the GPU output
+    on the same pixels: the bench's parity self-check.
+    """
+    from oracle import load_c_oracle  # test infrastructure: reported baseline / checker only
     import ctypes
     H, W, C, bits, _, _ = cfg
     dt = {8: np.uint8, 16: np.uint16, 32: np.uint32}[bits]
     threads = threads or len(os.sched_getaffinity(0))
     lib = load_c_oracle()
     rng = np.random.default_rng(1)
+    h = k // 2
     width = min(W, 2048)
+    cw = min(W, width + h)          # crop columns (left edge = the image edge)
+    valid_w = W if cw == W else cw - h
+    check = {"pixels": 0, "mismatches": 0}
 
-    def run(rows):
-        img = rng.integers(0, np.iinfo(dt).max, size=(rows, width), dtype=dt, endpoint=True)
-        out = np.empty_like(img)
+    def crop(rows):
+        y0 = max(0, H // 2 - rows // 2)
+        s0, s1 = max(0, y0 - h), min(H, y0 + rows + h)
+        if src is None:
+            img = rng.integers(0, np.iinfo(dt).max, size=(s1 - s0, cw, C), dtype=dt, endpoint=True)
+        else:
+            t = src[s0:s1, :cw]
+            img = t.cpu().numpy().astype(dt).reshape(s1 - s0, cw, C)
+        return y0, s0, img
+
+    def run(rows, verify=False):
+        y0, s0, img = crop(rows)
+        planes = [np.ascontiguousarray(img[..., c]) for c in range(C)]
+        outs = [np.empty((rows, cw), dtype=dt) for _ in range(C)]
         t0 = time.perf_counter()
-        for _ in range(C):
-            rc = lib.oracle_median2d(ctypes.c_void_p(img.ctypes.data), width,
-                                     ctypes.c_void_p(out.ctypes.data), width, width, rows,
-                                     bits, k, k, 0, rows, threads)
+        for c in range(C):
+            base = outs[c].ctypes.data - (y0 - s0) * cw * planes[c].itemsize
+            rc = lib.oracle_median2d(ctypes.c_void_p(planes[c].ctypes.data), cw,
+                                     ctypes.c_void_p(base), cw, cw, planes[c].shape[0],
+                                     bits, k, k, y0 - s0, y0 - s0 + rows, threads)
             assert rc == 0
-        return time.perf_counter() - t0
+        dt_s = time.perf_counter() - t0
+        if verify and ours is not None:
+            got = ours[y0:y0 + rows, :valid_w].cpu().numpy().astype(dt).reshape(rows, valid_w, C)
+            for c in range(C):
+                check["pixels"] += rows * valid_w
+                check["mismatches"] += int((got[..., c] != outs[c][:, :valid_w]).sum())
+        return dt_s
 
     rows = 8
     dt_s = run(rows)
@@ -177,16 +218,20 @@ def cpu_baseline(cfg, k, seconds=10.0, threads=None):
     # repeat the crop until `seconds` of work; report the median repetition
     reps, total = [], 0.0
     while total < seconds or len(reps) < 3:
-        t = run(rows)
+        t = run(rows, verify=not reps)
         reps.append(t)
         total += t
     dt_s = statistics.median(reps)
-    samples = rows * width * C
-    return {"value": samples / dt_s / 1e9, "unit": "Gpixel/s", "cores": threads, "kind": "port",
-            "sample": f"{rows}x{width}x{C} crop of the same workload (uint{bits}, k={k}), "
-                      f"median of {len(reps)} repetitions ({total:.1f} s total), "
-                      f"oracle/median_oracle.c with {threads} threads",
-            "seconds": round(total, 2)}
+    samples = rows * cw * C
+    res = {"value": samples / dt_s / 1e9, "unit": "Gpixel/s", "cores": threads, "kind": "port",
+           "cpu_model": cpu_model(),
+           "sample": f"{rows}x{cw}x{C} crop of the same workload (rows around the middle, "
+                     f"columns from the left edge; uint{bits}, k={k}), median of {len(reps)} "
+                     f"repetitions ({total:.1f} s total), oracle/median_oracle.c with {threads} threads",
+           "seconds": round(total, 2)}
+    if ours is not None:
+        res["parity_check"] = dict(check, rows=rows, columns=valid_w, channels=C)
+    return res
 
 
 def run_reference(args, cfg, k, rank, world):
@@ -210,9 +255,12 @@ def run_reference(args, cfg, k, rank, world):
         "ms_per_step": 1e3 * H * W * C / (v * 1e9),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": f"u{bits}", "data": "synthetic (uniform random)",
-        "config": {"workload": label, "k": k, "height": H, "width": W, "channels": C},
+        "config": {"workload": label, "k": k, "height": H, "width": W, "channels": C,
+                   "sample": times[-1]["sample"],
+                   "timing": "per step: the crop's median repetition, scaled to the full image "
+                             "(ms_per_step); per-pixel cost is size-independent"},
         "cpu_baseline": {"value": v, "unit": "Gpixel/s", "cores": threads, "kind": "port",
-                         "sample": times[-1]["sample"]},
+                         "cpu_model": cpu_model(), "sample": times[-1]["sample"]},
         "e2e": {"value": v, "unit": "Gpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -228,6 +276,8 @@ def main():
     ap.add_argument("--variant", default="auto")
     ap.add_argument("--mode", default=None, choices=("frames", "bands"))
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--pattern", default="random",
+                    help="synthetic input pattern (paper_2507_19926_b200.synth.PATTERNS)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
@@ -253,25 +303,22 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     from paper_2507_19926_b200 import _lib, bands, filter_planes
     from paper_2507_19926_b200.program import op_model
+    from paper_2507_19926_b200.synth import render
     lib = _lib.load()
     tdt = {8: torch.uint8, 16: torch.uint16, 32: torch.uint32}[bits]
     esz = bits // 8
 
     # ---- inputs resident in HBM ------------------------------------------
-    g = torch.Generator(device=dev).manual_seed(42 + rank)
-    hi = (1 << bits) if bits < 32 else (1 << 32)
     if mode == "bands":
         y0, y1 = bands.band_rows(H, world, rank)
         rows = y1 - y0
-        band = torch.randint(0, hi, (rows, W, C) if C > 1 else (rows, W), generator=g,
-                             device=dev, dtype=torch.int64).to(tdt)
+        band = render(args.pattern, (rows, W, C) if C > 1 else (rows, W), bits, 42 + rank, dev)
         halo = k // 2
         buf, r0 = bands.halo_buffer(band, halo, rank > 0, rank < world - 1)
         del band
         samples_rank = rows * W * C
     else:
-        img = torch.randint(0, hi, (H, W, C) if C > 1 else (H, W), generator=g, device=dev,
-                            dtype=torch.int64).to(tdt)
+        img = render(args.pattern, (H, W, C) if C > 1 else (H, W), bits, 42 + rank, dev)
         out = torch.empty_like(img)
         samples_rank = H * W * C
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
@@ -324,12 +371,35 @@ def main():
         samples_job = samples_rank * world
     value = samples_job * args.steps / (total_ms * 1e-3) / 1e9
 
-    # ---- end to end through the C ABI on pinned host buffers ----------------
+    # ---- end to end ------------------------------------------------------
+    # (1) the drop-in a user calls: filter_planes on a pageable numpy image ->
+    #     numpy (host staging + H2D + filter + D2H inside the call);
+    # (2) the C ABI on pinned host buffers (the copy engines' bound).
     e2e = None
+    e2e_pinned = None
     if mode == "frames":
+        nbytes = H * W * C * esz
+        host_np = img.cpu().numpy()  # pageable numpy, as a user's image would be
+        for _ in range(2):
+            filter_planes(host_np, k, variant, device=local)
+        if world > 1:
+            dist.barrier()
+        n_e2e = max(3, args.steps // 2)
+        t0 = time.perf_counter()
+        for _ in range(n_e2e):
+            res = filter_planes(host_np, k, variant, device=local)
+        e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        del res
+        if world > 1:
+            dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+        e2e = {"value": samples_rank * world * n_e2e / float(e2e_s.item()) / 1e9,
+               "unit": "Gpixel/s", "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+               "path": "filter_planes(numpy) drop-in: pageable input, pinned output, "
+                       "H2D + filter + D2H inside the call, wall clock"}
         hin = torch.empty(img.shape, dtype=tdt, pin_memory=True)
         hin.copy_(img)
         hout = torch.empty_like(hin).pin_memory()
+
         def host_step():
             rc = lib.tm_median2d_host(hin.data_ptr(), W * C * esz, hout.data_ptr(), W * C * esz,
                                       W, H, C, bits, k, k, vcode, local)
@@ -339,16 +409,15 @@ def main():
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
-        n_e2e = max(3, args.steps // 2)
         for _ in range(n_e2e):
             host_step()
         e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
-        nbytes = H * W * C * esz
-        e2e = {"value": samples_rank * world * n_e2e / float(e2e_s.item()) / 1e9,
-               "unit": "Gpixel/s", "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
-               "path": "tm_median2d_host (C ABI) on pinned host buffers, H2D + filter + D2H"}
+        e2e_pinned = {"value": samples_rank * world * n_e2e / float(e2e_s.item()) / 1e9,
+                      "unit": "Gpixel/s", "h2d_bytes_per_step": nbytes,
+                      "d2h_bytes_per_step": nbytes,
+                      "path": "tm_median2d_host (C ABI) on pinned host buffers"}
 
     if rank != 0:
         if world > 1:
@@ -369,49 +438,71 @@ def main():
     if os.path.exists(prof):
         with open(prof) as f:
             traffic = json.load(f).get("dram_bytes_per_launch")
-    roofline = {"bound": "alu" if k >= 5 else "hbm",
-                "achieved": alu_achieved, "peak": alu_peak, "unit": "T minmax/s",
-                "frac": alu_achieved / alu_peak, "traffic": traffic,
-                "kernel": kernel, "per_launch": f"W(k)={w_k:.1f} reference min/max per sample x "
-                f"{per_launch} samples", "peak_source": "measured (profiles/r01_minmax_microbench.txt)"}
-    # secondary: instruction issue of the dominant kernel -- ncu-measured warp
-    # instructions per sample (committed capture of this config) x the live
-    # sample rate, against 4 warp-instructions/clk/SM x 148 SMs x SM clock
+    roofline_model = {"bound": "alu", "achieved": alu_achieved, "peak": alu_peak,
+                      "unit": "T minmax/s", "frac": alu_achieved / alu_peak, "traffic": traffic,
+                      "kernel": kernel,
+                      "per_launch": f"W(k)={w_k:.1f} reference min/max per sample x "
+                                    f"{per_launch} samples (the reference's op model; the "
+                                    "data-aware kernels execute fewer operations)",
+                      "peak_source": "measured (profiles/r01_minmax_microbench.txt)"}
+    # hardware: instruction issue of the dominant kernel -- ncu-measured warp
+    # instructions per sample (committed capture of this config and kernel) x
+    # the live sample rate, against 4 warp-instructions/clk/SM x 148 SMs x the
+    # sampled SM clock
     roofline_issue = None
     ncu_prof = os.path.join(ROOT, "profiles", f"ncu_{args.config}_k{k}.json")
-    if os.path.exists(ncu_prof):
+    if os.path.exists(ncu_prof) and args.pattern == "random":
         with open(ncu_prof) as f:
             npf = json.load(f)
         ips = npf.get("warp_instructions_per_sample")
-        ncu_name = {"oblivious": "obl_kernel", "histogram": "hist8_kernel", "rank": "rank_kernel", "med3": "med3_kernel",
-                    "multipass": "aware", "select": "select"}.get(kernel, kernel)
+        ncu_name = {"oblivious": "obl_kernel", "histogram": "hist8_kernel", "rank": "rank_kernel",
+                    "med3": "med3_kernel", "multipass": "aware", "select": "select"}.get(kernel, kernel)
         if ips and ncu_name in npf.get("kernel", ""):
             clk_mhz = (clk.summary().get("sm_mhz") or 1965.0)
             achieved_wi = ips * per_launch / (kern_ms * 1e-3) / 1e12
             peak_wi = 4 * 148 * clk_mhz * 1e6 / 1e12
             roofline_issue = {"bound": "issue", "achieved": achieved_wi, "peak": peak_wi,
                               "unit": "T warp-instr/s", "frac": achieved_wi / peak_wi,
-                              "per_launch": f"{ips} warp instructions per sample (ncu, {ncu_prof[len(ROOT) + 1:]})"}
+                              "traffic": traffic, "kernel": kernel,
+                              "per_launch": f"{ips} warp instructions per sample (ncu, "
+                                            f"{ncu_prof[len(ROOT) + 1:]}) x {per_launch} samples",
+                              "peak_source": "4 warp-instr/clk/SM x 148 SMs x sampled SM clock"}
     roofline_hbm = {"bound": "hbm", "achieved": hbm_achieved, "peak": peaks.get("hbm_gbs"),
                     "unit": "GB/s", "frac": hbm_achieved / peaks.get("hbm_gbs", 6650.0),
-                    "traffic": traffic, "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+                    "traffic": traffic, "kernel": kernel,
+                    "per_launch": f"2 x {esz} B x {per_launch} samples",
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+    # primary: HBM for k = 3 (copy-bound), else the hardware issue roofline
+    # when a config-matched ncu capture exists, else the op model
     if k < 5:
-        roofline, roofline_hbm = roofline_hbm, roofline
+        roofline = roofline_hbm
+    elif roofline_issue is not None:
+        roofline = roofline_issue
+    else:
+        roofline = roofline_model
     line = {
         "metric": METRIC, "value": value, "unit": "Gpixel/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
         "higher_is_better": True, "scaling": "strong" if mode == "bands" else "weak",
-        "vs_baseline": None, "dtype": f"u{bits}", "data": "synthetic (uniform random, seeded)",
+        "vs_baseline": None, "dtype": f"u{bits}",
+        "data": f"synthetic ({args.pattern}, seeded; paper_2507_19926_b200.synth)",
         "config": {"workload": label, "k": k, "height": H, "width": W, "channels": C,
-                   "variant": variant, "kernel": kernel, "mode": mode,
+                   "variant": variant, "kernel": kernel, "mode": mode, "pattern": args.pattern,
                    "l2": "flushed (512 MiB write) before every timed step",
                    "parallelism": f"{mode} x{world}"},
-        "roofline": roofline, "roofline_hbm": roofline_hbm, "roofline_issue": roofline_issue,
-        "e2e": e2e,
+        "roofline": roofline, "roofline_model": roofline_model, "roofline_hbm": roofline_hbm,
+        "roofline_issue": roofline_issue,
+        "e2e": e2e, "e2e_pinned_cabi": e2e_pinned,
         "gpu_launches": int(launches), "clocks": clk.summary(),
     }
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(cfg, k)
+        # the reported CPU baseline, cut from this run's input; its result
+        # doubles as the parity self-check of this run's GPU output
+        line["cpu_baseline"] = cpu_baseline(cfg, k, src=img if mode == "frames" else None,
+                                            ours=out if mode == "frames" else None)
+        pc = line["cpu_baseline"].get("parity_check")
+        if pc is not None:
+            line["parity"] = "ok" if pc["mismatches"] == 0 else f"MISMATCH ({pc['mismatches']} px)"
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

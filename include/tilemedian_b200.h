@@ -11,6 +11,14 @@
  *                         455-491 bands re-reading +-k/2 halo rows): one band
  *                         of output rows from a source that carries its halo
  *   tm_median2d_host   <- filter_image on host (numpy) buffers, copies included
+ *   tm_median2d_host_multi <- filter_image(..., devices=[...]): one row band
+ *                         per GPU, each re-reading its k_h/2 halo rows (the
+ *                         reference's banding, aware.py:455-491)
+ *   tm_median2d_bands  <- the same banding on device-resident bands: halo rows
+ *                         exchanged between the GPUs (peer copies over NVLink)
+ *   tm_host_alloc/free <- the reference returns a fresh host array
+ *                         (oblivious.py:349); the drop-in returns it in pinned
+ *                         memory so the device-to-host copy runs at full speed
  *   tm_dispatch_query  <- pick_variant(k)                       engine.py:22-26
  *
  * Semantics (bit-exact with reference.py:26-43): out[y][x] is the rank
@@ -86,6 +94,35 @@ int tm_median2d_band(const void* src, int64_t src_pitch, int32_t src_rows,
 int tm_median2d_host(const void* src, int64_t src_pitch, void* dst, int64_t dst_pitch,
                      int32_t width, int32_t height, int32_t channels, int32_t bits,
                      int32_t k_w, int32_t k_h, int32_t variant, int32_t device);
+
+/* Host buffers split into n_dev balanced row bands, one per device in
+ * dev_ids, filtered concurrently (a repeated ordinal runs its bands one after
+ * the other); every device copies its
+ * own band plus k_h/2 halo rows from the host image, so the result is
+ * bit-identical to tm_median2d_host.  Synchronises. */
+int tm_median2d_host_multi(const void* src, int64_t src_pitch, void* dst, int64_t dst_pitch,
+                           int32_t width, int32_t height, int32_t channels, int32_t bits,
+                           int32_t k_w, int32_t k_h, int32_t variant, const int32_t* dev_ids,
+                           int32_t n_dev);
+
+/* Device-resident row bands of one image, band i (rows top to bottom) on
+ * device dev_ids[i].  band_buf[i] holds h = k_h/2 halo rows, then its
+ * band_rows[i] rows, then h halo rows (pitch band_pitch[i] bytes); the halo
+ * rows are filled here from the neighbouring bands (peer copies, NVLink when
+ * peer access is available) -- the first band's top and the last band's
+ * bottom halo are neither written nor read.  Output band i goes to
+ * band_dst[i] (band_rows[i] rows, pitch dst_pitch[i]) on streams[i] (NULL
+ * array = default streams); every band needs >= h rows when n_bands > 1.
+ * Stream-ordered; bit-identical to filtering the whole image on one GPU. */
+int tm_median2d_bands(void* const* band_buf, const int64_t* band_pitch, void* const* band_dst,
+                      const int64_t* dst_pitch, const int32_t* band_rows, const int32_t* dev_ids,
+                      int32_t n_bands, int32_t width, int32_t channels, int32_t bits,
+                      int32_t k_w, int32_t k_h, int32_t variant, void* const* streams);
+
+/* Pinned, portable host memory from a size-bucketed cache (NULL on failure);
+ * tm_host_free returns a block to the cache. */
+void* tm_host_alloc(int64_t bytes);
+int tm_host_free(void* p);
 
 /* Which kernel serves (bits, k_w, k_h, variant); TM_KERNEL_NONE if invalid. */
 int tm_dispatch_query(int32_t bits, int32_t k_w, int32_t k_h, int32_t variant);

@@ -33,6 +33,12 @@ _SIGS = {
                                         c_i32, c_i32, c_i32, c_i32, c_vp]),
     "tm_median2d_host": (ctypes.c_int, [c_vp, c_i64, c_vp, c_i64, c_i32, c_i32, c_i32, c_i32, c_i32,
                                         c_i32, c_i32, c_i32]),
+    "tm_median2d_host_multi": (ctypes.c_int, [c_vp, c_i64, c_vp, c_i64, c_i32, c_i32, c_i32, c_i32,
+                                              c_i32, c_i32, c_i32, c_vp, c_i32]),
+    "tm_median2d_bands": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32,
+                                         c_i32, c_i32, c_i32, c_i32, c_vp]),
+    "tm_host_alloc": (c_vp, [c_i64]),
+    "tm_host_free": (ctypes.c_int, [c_vp]),
     "tm_dispatch_query": (ctypes.c_int, [c_i32, c_i32, c_i32, c_i32]),
     "tm_kernel_name": (ctypes.c_char_p, [c_i32]),
     "tm_force_kernel": (ctypes.c_int, [c_i32]),

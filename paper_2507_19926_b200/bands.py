@@ -81,3 +81,47 @@ def filter_band(buf, out_row0: int, n_rows: int, k: int, variant: str = "auto"):
                                           W, ch, bits, k, k, _lib.VARIANT_CODES[v], stream)
     _lib.check(rc)
     return out
+
+
+def filter_sharded(image, kw: int, kh: int, variant: str, devices):
+    """Filter a CUDA tensor as one row band per GPU in ``devices`` (one process).
+
+    Every band is copied to its GPU into a buffer with k_h/2 halo rows of
+    slack on both sides; the C ABI's ``tm_median2d_bands`` fills the halos
+    from the neighbouring bands (peer copies over NVLink) and filters each
+    band on its own device and current stream.  The bands are gathered back on
+    the input's device, bit-identical to one GPU.
+    """
+    import ctypes
+
+    import torch
+    from . import _lib
+    bits = {torch.uint8: 8, torch.uint16: 16, torch.uint32: 32}[image.dtype]
+    H = int(image.shape[0])
+    halo = kh // 2
+    n = max(1, min(len(devices), H // max(halo, 1) if halo else H))
+    rest = tuple(image.shape[1:])
+    W = int(rest[0])
+    ch = 1 if image.ndim == 2 else int(rest[1])
+    esz = image.element_size()
+    bufs, outs, rows, ids, streams = [], [], [], [], []
+    for i in range(n):
+        y0, y1 = band_rows(H, n, i)
+        dev = torch.device("cuda", int(devices[i]))
+        buf = torch.empty((halo + (y1 - y0) + halo,) + rest, dtype=image.dtype, device=dev)
+        buf[halo:halo + y1 - y0].copy_(image[y0:y1])
+        bufs.append(buf)
+        outs.append(torch.empty((y1 - y0,) + rest, dtype=image.dtype, device=dev))
+        rows.append(y1 - y0)
+        ids.append(int(devices[i]))
+        streams.append(torch.cuda.current_stream(dev).cuda_stream)
+    arr = lambda ty, xs: (ty * n)(*xs)  # noqa: E731
+    rc = _lib.load().tm_median2d_bands(
+        arr(ctypes.c_void_p, [b.data_ptr() for b in bufs]),
+        arr(ctypes.c_int64, [b.stride(0) * esz for b in bufs]),
+        arr(ctypes.c_void_p, [o.data_ptr() for o in outs]),
+        arr(ctypes.c_int64, [o.stride(0) * esz for o in outs]),
+        arr(ctypes.c_int32, rows), arr(ctypes.c_int32, ids), n, W, ch, bits, kw, kh,
+        _lib.VARIANT_CODES[variant], arr(ctypes.c_void_p, streams))
+    _lib.check(rc)
+    return torch.cat([o.to(image.device) for o in outs], dim=0)

@@ -36,6 +36,17 @@ const tmb::OblEntry* find_obl(int bits, int k) {
   return nullptr;
 }
 
+int launch(int kernel, int bits, int k_w, int k_h, const tmb::Job& job, cudaStream_t s) {
+  switch (kernel) {
+    case TM_KERNEL_OBLIVIOUS: return find_obl(bits, k_w)->fn(job, s);
+    case TM_KERNEL_MULTIPASS: return tmb::launch_aware(bits, job, k_w, s);
+    case TM_KERNEL_HISTOGRAM: return tmb::launch_hist8(job, k_w, s);
+    case TM_KERNEL_RANK: return tmb::launch_rank(bits, job, k_w, s);
+    case TM_KERNEL_MED3: return tmb::launch_med3(bits, job, s);
+    default: return tmb::launch_select(bits, job, k_w, k_h, s);
+  }
+}
+
 // Kernel routing.  Results are identical whichever exact kernel runs; the
 // variant only chooses the algorithm (engine.py:36-52).
 bool supports(int kernel, int bits, int kw, int kh) {
@@ -102,6 +113,16 @@ int check_common(int width, int rows, int bits, int kw, int kh, int variant) {
 
 }  // namespace
 
+namespace tmb {
+int set_error(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+}  // namespace tmb
+
 extern "C" {
 
 int tm_median2d_band(const void* src, int64_t src_pitch, int32_t src_rows, int32_t out_row0,
@@ -132,30 +153,20 @@ int tm_median2d_band(const void* src, int64_t src_pitch, int32_t src_rows, int32
   job.out_h = out_rows;
   job.channels = channels;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  int err;
-  switch (route(bits, k_w, k_h, variant)) {
-    case TM_KERNEL_OBLIVIOUS:
-      err = find_obl(bits, k_w)->fn(job, s);
-      break;
-    case TM_KERNEL_MULTIPASS:
-      err = tmb::launch_aware(bits, job, k_w, s);
-      break;
-    case TM_KERNEL_HISTOGRAM:
-      err = tmb::launch_hist8(job, k_w, s);
-      break;
-    case TM_KERNEL_RANK:
-      err = tmb::launch_rank(bits, job, k_w, s);
-      break;
-    case TM_KERNEL_MED3:
-      err = tmb::launch_med3(bits, job, s);
-      break;
-    default:
-      err = tmb::launch_select(bits, job, k_w, k_h, s);
-      break;
+  const int kernel = route(bits, k_w, k_h, variant);
+  // at most 65535 output rows per launch (grid.y of the row-tiled kernels);
+  // taller images are launched in row chunks of the same source
+  constexpr int kMaxLaunchRows = 65535;
+  for (int r0 = 0; r0 < out_rows; r0 += kMaxLaunchRows) {
+    tmb::Job part = job;
+    part.out_y0 = out_row0 + r0;
+    part.out_h = std::min(kMaxLaunchRows, out_rows - r0);
+    part.dst = static_cast<char*>(dst) + (int64_t)r0 * dst_pitch;
+    const int err = launch(kernel, bits, k_w, k_h, part, s);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (err != cudaSuccess)
+      return fail(TM_ECUDA, "CUDA launch failed: %s", cudaGetErrorString((cudaError_t)err));
   }
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  if (err != cudaSuccess)
-    return fail(TM_ECUDA, "CUDA launch failed: %s", cudaGetErrorString((cudaError_t)err));
   return TM_OK;
 }
 
@@ -177,116 +188,6 @@ int tm_median2d_planes(const void* src, int64_t src_pitch, void* dst, int64_t ds
                        int32_t variant, void* stream) {
   return tm_median2d_band(src, src_pitch, height, 0, height, dst, dst_pitch, width, channels, bits,
                           k, k, variant, stream);
-}
-
-int tm_median2d_host(const void* src, int64_t src_pitch, void* dst, int64_t dst_pitch,
-                     int32_t width, int32_t height, int32_t channels, int32_t bits, int32_t k_w,
-                     int32_t k_h, int32_t variant, int32_t device) {
-  int rc = check_common(width, height, bits, k_w, k_h, variant);
-  if (rc) return rc;
-  if (!src || !dst) return fail(TM_EINVAL, "null buffer");
-  if (channels < 1) return fail(TM_EINVAL, "bad channel count %d", channels);
-  const int64_t row = (int64_t)width * channels * (bits / 8);
-  if (src_pitch < row || dst_pitch < row) return fail(TM_EINVAL, "pitch smaller than a row");
-  // Row bands pipelined over streams: band b's H2D copy, the filters of
-  // earlier bands (three filter streams, so band kernels overlap each other's
-  // tails) and their D2H copies run concurrently (PCIe is full duplex), so the
-  // call costs about max(H2D, filter, D2H) instead of their sum.  A band's
-  // filter waits for the input chunk holding its last halo row.
-  constexpr int kMaxBands = 32;
-  constexpr int kFilterStreams = 3;  // band kernels overlap each other's tails
-  struct Scratch {
-    void* buf = nullptr;
-    size_t bytes = 0;
-    cudaStream_t st[3] = {nullptr, nullptr, nullptr};  // h2d, filter, d2h
-    cudaStream_t fs[kFilterStreams] = {};               // concurrent band filters
-    cudaEvent_t ev_in[kMaxBands] = {}, ev_out[kMaxBands] = {};
-  };
-  static thread_local std::vector<Scratch> per_dev;
-  if (device < 0) return fail(TM_EINVAL, "bad device %d", device);
-  if ((int)per_dev.size() <= device) per_dev.resize(device + 1);
-  cudaError_t e = cudaSetDevice(device);
-  if (e != cudaSuccess) return fail(TM_ECUDA, "cudaSetDevice: %s", cudaGetErrorString(e));
-  Scratch& sc = per_dev[device];
-  const size_t need = 2 * (size_t)row * height;
-  if (sc.bytes < need) {
-    if (sc.buf) cudaFree(sc.buf);
-    sc.buf = nullptr;
-    sc.bytes = 0;
-    e = cudaMalloc(&sc.buf, need);
-    if (e != cudaSuccess) return fail(TM_ECUDA, "cudaMalloc: %s", cudaGetErrorString(e));
-    sc.bytes = need;
-  }
-  if (!sc.st[0]) {
-    for (auto& st : sc.st) {
-      e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
-      if (e != cudaSuccess) return fail(TM_ECUDA, "cudaStreamCreate: %s", cudaGetErrorString(e));
-    }
-    for (auto& st : sc.fs) {
-      e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
-      if (e != cudaSuccess) return fail(TM_ECUDA, "cudaStreamCreate: %s", cudaGetErrorString(e));
-    }
-    for (int b = 0; b < kMaxBands; b++) {
-      e = cudaEventCreateWithFlags(&sc.ev_in[b], cudaEventDisableTiming);
-      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&sc.ev_out[b], cudaEventDisableTiming);
-      if (e != cudaSuccess) return fail(TM_ECUDA, "cudaEventCreate: %s", cudaGetErrorString(e));
-    }
-  }
-  char* din = static_cast<char*>(sc.buf);
-  char* dout = din + (size_t)row * height;
-  const int halo = k_h / 2;
-  // bands of >= 64 rows and >= 2 MB, at most 16 (measured on C2: 1 -> 19.3,
-  // 4 -> 27.8, 8 -> 34.7, 16 -> 38.7, 32 -> 35.5 Gpixel/s e2e); small images
-  // get one band -- the pipeline only pays once copies dominate
-  const int64_t img_bytes = row * height;
-  static const int force_nb = [] {  // experiments: TMB_HOST_BANDS
-    const char* v = getenv("TMB_HOST_BANDS");
-    return v ? atoi(v) : 0;
-  }();
-  const int nb = force_nb > 0 ? std::min(std::min(force_nb, kMaxBands), height)
-                              : (int)std::max<int64_t>(1, std::min<int64_t>(
-                                    {16, height / 64, img_bytes / (2 << 20)}));
-  int y[kMaxBands + 1];
-  for (int b = 0; b <= nb; b++) y[b] = (int)((int64_t)height * b / nb);
-  const char* hsrc = static_cast<const char*>(src);
-  char* hdst = static_cast<char*>(dst);
-  for (int b = 0; b < nb; b++) {
-    const size_t n_rows = (size_t)(y[b + 1] - y[b]);
-    e = src_pitch == row
-            ? cudaMemcpyAsync(din + (size_t)y[b] * row, hsrc + (int64_t)y[b] * src_pitch,
-                              n_rows * row, cudaMemcpyHostToDevice, sc.st[0])
-            : cudaMemcpy2DAsync(din + (size_t)y[b] * row, row, hsrc + (int64_t)y[b] * src_pitch,
-                                src_pitch, row, n_rows, cudaMemcpyHostToDevice, sc.st[0]);
-    if (e == cudaSuccess) e = cudaEventRecord(sc.ev_in[b], sc.st[0]);
-    if (e != cudaSuccess) return fail(TM_ECUDA, "H2D copy: %s", cudaGetErrorString(e));
-  }
-  for (int b = 0; b < nb; b++) {
-    cudaStream_t fst = sc.fs[b % kFilterStreams];
-    const int last_src = std::min(height, y[b + 1] + halo) - 1;
-    int chunk = b;
-    while (chunk + 1 < nb && y[chunk + 1] <= last_src) chunk++;
-    e = cudaStreamWaitEvent(fst, sc.ev_in[chunk], 0);
-    if (e != cudaSuccess) return fail(TM_ECUDA, "stream wait: %s", cudaGetErrorString(e));
-    rc = tm_median2d_band(din, row, height, y[b], y[b + 1] - y[b], dout + (size_t)y[b] * row, row,
-                          width, channels, bits, k_w, k_h, variant, fst);
-    if (rc) return rc;
-    e = cudaEventRecord(sc.ev_out[b], fst);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(sc.st[2], sc.ev_out[b], 0);
-    if (e == cudaSuccess)
-      e = dst_pitch == row
-              ? cudaMemcpyAsync(hdst + (int64_t)y[b] * dst_pitch, dout + (size_t)y[b] * row,
-                                (size_t)(y[b + 1] - y[b]) * row, cudaMemcpyDeviceToHost, sc.st[2])
-              : cudaMemcpy2DAsync(hdst + (int64_t)y[b] * dst_pitch, dst_pitch,
-                                  dout + (size_t)y[b] * row, row, row, y[b + 1] - y[b],
-                                  cudaMemcpyDeviceToHost, sc.st[2]);
-    if (e != cudaSuccess) return fail(TM_ECUDA, "D2H copy: %s", cudaGetErrorString(e));
-  }
-  e = cudaStreamSynchronize(sc.st[2]);
-  for (auto& st : sc.fs)
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(sc.st[0]);
-  if (e != cudaSuccess) return fail(TM_ECUDA, "kernel failed: %s", cudaGetErrorString(e));
-  return TM_OK;
 }
 
 int tm_dispatch_query(int32_t bits, int32_t k_w, int32_t k_h, int32_t variant) {

@@ -9,7 +9,9 @@
 // 8-bit data is widened to 16-bit lanes (sm_100a has no native u8x4 min/max:
 // __vminu4 lowers to LOP3/PRMT sequences -- profiles/r01_minmax_microbench.txt).
 #pragma once
+#include <atomic>
 #include <cstdint>
+#include <mutex>
 #include <cuda_runtime.h>
 
 namespace tmb {
@@ -126,8 +128,9 @@ __device__ __forceinline__ void store_row(const Job& job, int y, int x0, const T
     if (x0 + i < job.width) store_px<T>(job, y, x0 + i, v[i]);
 }
 
-// Per-kernel launch facts, computed once (C++11 thread-safe static init at
-// the call site): opt-in shared-memory limit, SM count, resident CTAs per SM.
+// Per-kernel launch facts: opt-in shared-memory limit, SM count, resident CTAs
+// per SM.  The shared-memory attribute is per device context, so the facts are
+// kept per device ordinal (LaunchCache); a failed query is not cached.
 struct LaunchInfo {
   cudaError_t err;
   int sms;
@@ -146,5 +149,29 @@ inline LaunchInfo launch_info(F fn, int threads, int smem) {
   li.occ = o > 0 ? o : 1;
   return li;
 }
+
+// One per launcher (function-local static): launch facts per device ordinal,
+// computed on the first launch on that device, thread-safe.
+struct LaunchCache {
+  static constexpr int kMaxDev = 64;
+  std::atomic<int> ready[kMaxDev] = {};
+  LaunchInfo info[kMaxDev] = {};
+  std::mutex mu;
+  template <typename F>
+  LaunchInfo get(F fn, int threads, int smem) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev)
+      return launch_info(fn, threads, smem);
+    if (ready[dev].load(std::memory_order_acquire)) return info[dev];
+    std::lock_guard<std::mutex> g(mu);
+    if (!ready[dev].load(std::memory_order_relaxed)) {
+      const LaunchInfo li = launch_info(fn, threads, smem);
+      if (li.err != cudaSuccess) return li;  // not cached: a later call retries
+      info[dev] = li;
+      ready[dev].store(1, std::memory_order_release);
+    }
+    return info[dev];
+  }
+};
 
 }  // namespace tmb

@@ -173,7 +173,8 @@ int launch_hist8_k(const Job& job, cudaStream_t stream) {
   constexpr int kSmem = C::kWarpBytes * WPC;
   static_assert(kSmem <= 227 * 1024, "histogram kernel does not fit in shared memory");
   auto fn = hist8_kernel<K, G, WPC>;
-  static const LaunchInfo li = launch_info(fn, 32 * WPC, kSmem);
+  static LaunchCache cache;
+  const LaunchInfo li = cache.get(fn, 32 * WPC, kSmem);
   if (li.err != cudaSuccess) return (int)li.err;
   const int sms = li.sms, occ = li.occ;
   const int n_strips = (job.width + C::S::COLS - 1) / C::S::COLS;

@@ -189,12 +189,10 @@ __global__ void __launch_bounds__(NT) med3_kernel(Job job, int R, int n_tx, int 
 template <typename T>
 int launch_med3_t(const Job& job, cudaStream_t stream) {
   constexpr int L = M3<T>::L;
-  static const int sms = [] {
-    int dev = 0, n = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    return n > 0 ? n : 148;
-  }();
+  static LaunchCache cache;
+  const LaunchInfo li = cache.get(med3_kernel<T>, NT, 0);
+  if (li.err != cudaSuccess) return (int)li.err;
+  const int sms = li.sms;
   const int n_tx = (job.width + TX - 1) / TX;
   // rows per strip: enough threads for ~4 full waves of 2048 threads/SM, at
   // least 1 row (small images: parallelism over the 2 re-read halo rows)
@@ -210,6 +208,8 @@ int launch_med3_t(const Job& job, cudaStream_t stream) {
   const int vb = 8 * (int)sizeof(T) > 16 ? 16 : 8 * (int)sizeof(T);  // vector alignment needed
   const int vec_ok = job.channels == 1 && base_s % vb == 0 && base_d % vb == 0 &&
                      (job.src_pitch * sizeof(T)) % vb == 0 && (job.dst_pitch * sizeof(T)) % vb == 0;
+  // grid.y is capped at 65535 row strips: tall narrow images get longer strips
+  while ((job.out_h + L * R - 1) / (L * R) > 65535) R *= 2;
   dim3 grid((unsigned)(((n_tx + NT - 1) / NT) * job.channels),
             (unsigned)((job.out_h + L * R - 1) / (L * R)));
   med3_kernel<T><<<grid, NT, 0, stream>>>(job, (int)R, n_tx, vec_ok);

@@ -7,25 +7,20 @@
 // selected exactly by rank among the survivors (the paper's forgetful
 // candidate windows, section 5.1, applied per tile of outputs).
 //
-// One warp = one work item: 64 output columns x up to RMAX output rows.
-//  1. coarse pass: sweep with key = the top 7 bits of each sample.  Gives every
-//     output pixel the exact 7-bit prefix of its median; every median of the
-//     item lies in [lo, hi] = [B_lo << s, ((B_hi + 1) << s) - 1].
-//  2. fine keys: 0 below lo, 127 above hi, 1 + floor((v - lo) * 125 / span)
-//     inside (value-width bins, monotone in v, computed from the value alone;
-//     one value per bin when the span is at most 125).  When bins hold several
-//     values the
-//     candidates (samples in [lo, hi]) are bucketed by key (count, exclusive
-//     scan, place) and each bucket is sorted by value, so bin b's candidates
-//     are the sorted range [start[b], start[b+1]).
-//  3. fine pass: sweep over the fine keys.  The walk lands every pixel in a bin
-//     b with residual rank r' = R2 - #keys < b; the median is lo + b - 1 for
-//     one-value bins, else the r'-th candidate of bin b (in sorted order) inside the
-//     pixel's window.
-// Exact by construction.  If an item has more candidates than fit (CMAX) it
-// is split in halves by rows (down to single rows); a row that still does not
-// fit is selected per pixel by brute force (radix selection over the window)
-// -- only adversarial high-entropy data gets there.
+// One warp = one work item: 64 output columns x up to RMAX output rows.  Every
+// pass is a sweep of the shared sliding histogram (tm_sweep.cuh) over 7-bit
+// keys; what changes between passes is the key function (KeyFn below):
+//  * range sweep: key = the position of each sample inside the footprint's own
+//    value range [fmin, fmax] (7 bits) -> every median of the item lies in the
+//    union [lo, hi] of the bins the pixels' walks end in;
+//  * candidate fine sweep (few samples inside an interval [lo, hi]): keys 0
+//    below lo, 127 above hi, 1 + floor((v - lo) * 126 / span) inside; the
+//    candidates are bucketed by key and sorted, so the walk's bucket plus its
+//    residual rank picks the median among the bucket's in-window candidates;
+//  * exact slices (one value per bin over 126 values): the walk's bin is the
+//    median.
+// Exact by construction for every input; the per-item decisions are described
+// above rank_kernel.
 #pragma once
 #include <cstdint>
 #include <cstdlib>
@@ -41,12 +36,7 @@ namespace {
 
 template <typename T, int K>
 struct RankCfg {
-#ifndef TMB_RANK_FINE_BINS
-#define TMB_RANK_FINE_BINS 128
-#endif
-  static constexpr int NBC = 128;                      // coarse key bins (top 7 bits)
-  static constexpr int NB = TMB_RANK_FINE_BINS;        // fine key bins
-  using SWC = WarpSweep<K, NBC>;
+  static constexpr int NB = 128;                       // key bins (7-bit keys)
   using SW = WarpSweep<K, NB>;
 #ifndef TMB_RANK_BIG_RMAX
 #define TMB_RANK_BIG_RMAX 128
@@ -70,11 +60,10 @@ struct RankCfg {
       K <= 45 ? 2048 : (sizeof(T) == 2 && K <= 53 ? 3072 : TMB_RANK_BIG_CMAX);  // measured
   static constexpr int kValBytes = CMAX * (int)sizeof(T);
   static constexpr int kPosBytes = CMAX * 2;
-  static constexpr int kStartBytes = (NB + 16) * 4;      // start[]
-  static constexpr int kHistBytes = SW::kHistBytes > SWC::kHistBytes ? SW::kHistBytes : SWC::kHistBytes;
+  static constexpr int kStack = 16;                    // pending value intervals
+  static constexpr int kStartBytes = ((NB + 1) + 3 * kStack + 3) * 4;  // start[], interval stack
+  static constexpr int kHistBytes = SW::kHistBytes;
   static constexpr int kWarpBytes = kHistBytes + kRingBytes + kValBytes + kPosBytes + kStartBytes;
-  static constexpr int BITS = 8 * (int)sizeof(T);
-  static constexpr int SHIFT = BITS - 7;               // coarse key = top 7 bits (NBC)
   static constexpr int E = (G * FW + 31) / 32;         // prefetch samples per lane
 };
 
@@ -83,45 +72,41 @@ __device__ __forceinline__ uint32_t load_s(const T* src, const Job& job, int y, 
   return __ldg(src + (int64_t)y * job.src_pitch + (int64_t)x * job.channels);
 }
 
-// Brute-force exact median of one pixel (last-resort path): MSB-first radix
-// selection over the clamped window, one bit per pass.
-template <typename T, int K>
-__device__ uint32_t brute_median(const T* src, const Job& job, int yc, int xc) {
-  constexpr int R2 = (K * K + 1) / 2;
-  uint32_t prefix = 0, need = R2;
-  for (int bit = 8 * (int)sizeof(T) - 1; bit >= 0; bit--) {
-    const uint32_t hi_mask = bit + 1 >= 32 ? 0u : (~0u << (bit + 1));
-    uint32_t zeros = 0;
-    for (int dy = -K / 2; dy <= K / 2; dy++) {
-      const int y = clampi(yc + dy, 0, job.src_h - 1);
-      for (int dx = -K / 2; dx <= K / 2; dx++) {
-        const uint32_t v = load_s(src, job, y, clampi(xc + dx, 0, job.width - 1));
-        zeros += ((v & hi_mask) == prefix) && !((v >> bit) & 1u);
-      }
-    }
-    if (need > zeros) {
-      need -= zeros;
-      prefix |= 1u << bit;
-    }
-  }
-  return prefix;
-}
-
-// Key of a sample: coarse pass (f < 0): top 7 bits; fine pass: 0 / NB-1 outside
-// [lo, hi], 1 + floor((v - lo) * (NB - 2) / span) inside.
+// Key of a sample.
+//   f < 0  (range pass):    (v - lo) >> shift clamped to [0, NB-1] -- the 7-bit
+//                           position of v inside a guess of the footprint's own
+//                           value range (adaptive: narrow or smooth data
+//                           spreads over all bins; outliers clamp to the ends);
+//   f == 0 (exact slice):   0 below lo, NB-1 above hi, 1 + v - lo inside (one
+//                           value per bin, hi - lo <= NB - 3);
+//   f > 0  (interval pass): 0 / NB-1 outside [lo, hi], 1 + floor((v - lo) *
+//                           (NB - 2) / span) inside (monotone in v).
 template <int NB>
 struct KeyFn {
   uint32_t lo, hi;
-  uint32_t mul;  // fine: bin = (v - lo) * mul >> 32, all NB - 2 inner bins in use
-  int f;         // < 0: coarse; 0: one value per bin; > 0: multi-value bins
+  uint32_t mul;  // f > 0: bin = (v - lo) * mul >> 32, all NB - 2 inner bins in use
+  int f;
   int shift;
   __device__ __forceinline__ uint8_t operator()(uint32_t v) const {
-    if (f < 0) return (uint8_t)(v >> shift);
+    if (f < 0) return v < lo ? 0 : (uint8_t)min((v - lo) >> shift, (uint32_t)(NB - 1));
     if (v < lo) return 0;
     if (v > hi) return NB - 1;
     return (uint8_t)(1 + (f == 0 ? v - lo : __umulhi(v - lo, mul)));
+  }  // f > 0: the smallest value whose key is >= b (1 <= b <= NB - 1); hi + 1
+  // (mod 2^32) when no value of [lo, hi] gets there.  Exact: key(v) >= b iff
+  // (v - lo) * mul >= (b - 1) * 2^32.
+  __device__ __forceinline__ uint32_t first_of(int b) const {
+    const uint64_t d = (((uint64_t)(b - 1) << 32) + mul - 1) / mul;
+    return d <= (uint64_t)(hi - lo) ? lo + (uint32_t)d : hi + 1u;
   }
 };
+
+__device__ __forceinline__ uint32_t warp_min(uint32_t v) {
+  return __reduce_min_sync(0xffffffffu, v);
+}
+__device__ __forceinline__ uint32_t warp_max(uint32_t v) {
+  return __reduce_max_sync(0xffffffffu, v);
+}
 
 #ifdef TMB_RANK_PROFILE
 static __device__ unsigned long long g_rank_prof[8];  // per translation unit; tm_rank.cu sums them
@@ -130,19 +115,40 @@ static __device__ unsigned long long g_rank_prof[8];  // per translation unit; t
 #define RANK_T(i) do { } while (0)
 #endif
 
+// Per item (64 columns x R output rows) the kernel finds value intervals that
+// hold every median of the item and resolves each exactly, the cheapest way
+// the scans' counts allow -- so smooth, constant, narrow-range and impulse
+// data cost a small constant factor of random data, never a per-pixel path:
+//   0. footprint scan: [fmin, fmax].  At most NB - 2 distinct values -> one
+//      exact slice sweep (constant and near-constant data);
+//   1. range sweep on 7-bit positions in [fmin, fmax] -> the interval [lo, hi]
+//      of the bins the medians landed in;
+//   2. per interval: count scan of its candidates (samples inside) over 126
+//      fine buckets.  If they fit (CMAX): place, sort, fine sweep (random-like
+//      data: concentrated medians).  Otherwise the medians are spread: exact
+//      slices of 126 values when the candidates' range is short (gradients,
+//      impulse noise over them); a recount when that range is much narrower;
+//      else consecutive buckets are grouped to fit CMAX, one fine sweep per
+//      group, and a bucket that alone overflows becomes an interval of its own
+//      (126 finer buckets; intervals pend on a small stack).
+// Every pixel's median lies in exactly one resolved bucket or slice, and each
+// pass stores only the pixels whose median it resolves.
 template <typename T, int K>
-__global__ void __launch_bounds__(32) rank_kernel(Job job, int R, int n_strips, int n_segs) {
+__global__ void __launch_bounds__(32, 1) rank_kernel(Job job, int R, int n_strips, int n_segs) {
   using C = RankCfg<T, K>;
   using SW = typename C::SW;
+  constexpr int NB = C::NB;
+  constexpr uint32_t kInner = NB - 2;  // inner bins of a key
+  constexpr int kStack = C::kStack;
   extern __shared__ __align__(16) uint32_t smem[];
   const int lane = threadIdx.x;
   uint8_t* ring = reinterpret_cast<uint8_t*>(smem) + C::kHistBytes;
   T* cval = reinterpret_cast<T*>(ring + C::kRingBytes);                  // bucketed candidates
   uint16_t* cpos = reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(cval) + C::kValBytes);
   int* start = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(cpos) + C::kPosBytes);
-  typename C::SWC swc;  // coarse and fine sweeps share the histogram words
+  uint32_t* stk = reinterpret_cast<uint32_t*>(start + NB + 1);          // interval stack
+  int* cur = reinterpret_cast<int*>(smem);  // placement cursors: idle histogram words
   SW sw;
-  swc.init(smem, lane);
   sw.init(smem, lane);
   const int W = job.width, SH = job.src_h, CH = job.channels;
   const int n_items = n_strips * CH * n_segs;
@@ -158,10 +164,9 @@ __global__ void __launch_bounds__(32) rank_kernel(Job job, int R, int n_strips, 
     T* dst = static_cast<T*>(job.dst) + chan;
     const int x = X0 + 2 * lane;
 
-    int Rcur = rows_item;
-    for (int y0 = 0; y0 < rows_item;) {
-      const int rows = min(Rcur, rows_item - y0);
-      const int Y0 = Yi + y0;
+    {
+      const int rows = rows_item;
+      const int Y0 = Yi;
       const int sy_base = job.out_y0 + Y0 - C::H;  // source row of footprint row 0
       const int q_end = K + rows - 1;              // footprint rows
 
@@ -188,14 +193,20 @@ __global__ void __launch_bounds__(32) rank_kernel(Job job, int R, int n_strips, 
       };
 
       // One sweep over the sub-item with keys from `kf`; `emit(t)` after each row.
-      auto sweep = [&](auto& sw, const auto& kf, auto&& emit) {
-        using S = typename std::remove_reference<decltype(sw)>::type;
+      uint32_t fmin = 0xFFFFFFFFu, fmax = 0u;  // the footprint's value range (lane-partial)
+      auto sweep = [&](const KeyFn<NB>& kf, auto&& emit, bool track = false) {
         auto stash = [&](int q0, const uint32_t (&v)[C::E]) {
 #pragma unroll
           for (int e = 0; e < C::E; e++) {
             const int idx = lane + e * 32;
             const int g = idx / C::FW, c = idx - (idx / C::FW) * C::FW;
-            if (valid(q0, e)) ring[((q0 + g) % C::RING) * C::KW + c] = kf(v[e]);
+            if (valid(q0, e)) {
+              ring[((q0 + g) % C::RING) * C::KW + c] = kf(v[e]);
+              if (track) {  // every footprint sample is stashed exactly once
+                fmin = min(fmin, v[e]);
+                fmax = max(fmax, v[e]);
+              }
+            }
           }
         };
         auto row = [&](int q) { return ring + (q % C::RING) * C::KW; };
@@ -216,8 +227,8 @@ __global__ void __launch_bounds__(32) rank_kernel(Job job, int R, int n_strips, 
         sw.zero();
         __syncwarp();
         for (int q = 0; q < K; q++) {
-          uint32_t ch[S::NC];
-          S::chunks(row(q), lane, ch);
+          uint32_t ch[SW::NC];
+          SW::chunks(row(q), lane, ch);
           sw.add_row(ch);
         }
         sw.init_median();
@@ -228,9 +239,9 @@ __global__ void __launch_bounds__(32) rank_kernel(Job job, int R, int n_strips, 
           if (qn < q_end) fetch_raw(qn, nxt);
           const int t1 = min(t0 + C::G, rows);
           for (int t = t0; t < t1; t++) {
-            uint32_t co[S::NC], ci[S::NC];
-            S::chunks(row(t - 1), lane, co);
-            S::chunks(row(t - 1 + K), lane, ci);
+            uint32_t co[SW::NC], ci[SW::NC];
+            SW::chunks(row(t - 1), lane, co);
+            SW::chunks(row(t - 1 + K), lane, ci);
             sw.step(co, ci);
             emit(t);
           }
@@ -238,114 +249,92 @@ __global__ void __launch_bounds__(32) rank_kernel(Job job, int R, int n_strips, 
           __syncwarp();
         }
       };
-
-#ifdef TMB_RANK_PROFILE
-      long long _t = clock64();
-#endif
-      // ---- 1. candidate range: the exact coarse pass ------------------------
-      uint32_t lo, hi;
-      {
-        int blo = C::NBC - 1, bhi = 0;
-        KeyFn<C::NBC> kc{0u, 0u, 0u, -1, C::SHIFT};
-        sweep(swc, kc, [&](int) {
+      // Every EVERY-th footprint row (G = 1): visit(v, pos).
+      auto scan_rows = [&](int every, auto&& visit) {
+        for (int q0 = 0; q0 < q_end; q0 += every) {
+          uint32_t va[C::E];
+          fetch_raw(q0, va);
+#pragma unroll
+          for (int e = 0; e < C::E; e++)
+            if (valid(q0, e)) visit(va[e], pos_of(q0, e));
+        }
+      };
+      // Every footprint sample once (loads double-buffered): visit(v, pos).
+      auto scan = [&](auto&& visit) {
+        uint32_t va[C::E], vb[C::E];
+        fetch_raw(0, va);
+        auto visit_all = [&](int q0, const uint32_t (&v)[C::E]) {
+#pragma unroll
+          for (int e = 0; e < C::E; e++)
+            if (valid(q0, e)) visit(v[e], pos_of(q0, e));
+        };
+        int q0 = 0;
+        for (; q0 + C::G < q_end; q0 += 2 * C::G) {
+          fetch_raw(q0 + C::G, vb);
+          visit_all(q0, va);
+          if (q0 + 2 * C::G < q_end) fetch_raw(q0 + 2 * C::G, va);
+          visit_all(q0 + C::G, vb);
+        }
+        if (q0 < q_end) visit_all(q0, va);
+      };
+      auto put = [&](int t, int c, uint32_t v) {
+        if (x + c < W) dst[(int64_t)(Y0 + t) * job.dst_pitch + (int64_t)(x + c) * CH] = (T)v;
+      };
+      // Bins [blo, bhi] holding the medians of the sub-item's in-image columns.
+      auto range_pass = [&](const KeyFn<NB>& kf, int& blo, int& bhi) {
+        int b0 = NB - 1, b1 = 0;
+        sweep(kf, [&](int) {
           if (x < W) {
-            blo = min(blo, swc.m[0]);
-            bhi = max(bhi, swc.m[0]);
+            b0 = min(b0, sw.m[0]);
+            b1 = max(b1, sw.m[0]);
           }
           if (x + 1 < W) {
-            blo = min(blo, swc.m[1]);
-            bhi = max(bhi, swc.m[1]);
+            b0 = min(b0, sw.m[1]);
+            b1 = max(b1, sw.m[1]);
           }
         });
-        for (int o = 16; o; o >>= 1) {
-          blo = min(blo, __shfl_xor_sync(0xffffffffu, blo, o));
-          bhi = max(bhi, __shfl_xor_sync(0xffffffffu, bhi, o));
-        }
-        lo = (uint32_t)blo << C::SHIFT;
-        hi = (uint32_t)(((uint64_t)(bhi + 1) << C::SHIFT) - 1);
-      }
-      // value -> fine bin: identity when [lo, hi] has at most NB - 2 values,
-      // else floor((v - lo) * (NB - 2) / (hi - lo + 1)) via a 32.32 multiplier
-      const uint64_t span = (uint64_t)(hi - lo) + 1;
-      const int f = span <= (uint64_t)(C::NB - 2) ? 0 : 1;
-      const uint32_t mul = f ? (uint32_t)((((uint64_t)(C::NB - 2)) << 32) / span) : 0u;
-      const KeyFn<C::NB> kf{lo, hi, mul, f, 0};
+        blo = (int)warp_min((uint32_t)b0);
+        bhi = (int)warp_max((uint32_t)b1);
+      };
+      // Exact slice: one value per bin over [a, b] (b - a < NB - 2); stores
+      // every pixel whose median lies in [a, b].
+      auto slice = [&](uint32_t a, uint32_t b) {
+        const KeyFn<NB> kx{a, b, 0u, 0, 0};
+        sweep(kx, [&](int t) {
+#pragma unroll
+          for (int c = 0; c < 2; c++) {
+            const int bb = sw.m[c];
+            if (bb >= 1 && bb <= NB - 2) put(t, c, a + (uint32_t)(bb - 1));
+          }
+        });
+      };
+      auto slices = [&](uint32_t a, uint32_t b) {
+        for (uint64_t s0 = a; s0 <= b; s0 += kInner)
+          slice((uint32_t)s0, (uint32_t)min((uint64_t)b, s0 + kInner - 1));
+      };
 
-      RANK_T(0);
-      // ---- 2. candidates bucketed by fine key (only when f > 0) ----------
-      // Two scans of the footprint: count per key, then place each candidate
-      // at its bucket's cursor; each bucket is then sorted by value.
-      int n_cand = 0;
-      if (f > 0) {
-        // lane-private bucket counters in the (idle) histogram words:
-        // counter (bucket, lane) at word bucket * 32 + lane -- no contention
-        uint32_t* lc = smem;
-        for (int b = 0; b < C::NB; b++) lc[b * 32 + lane] = 0;
+      // Candidates of buckets [ba, bb] of `kf` (they fit: start[bb + 1] -
+      // start[ba] <= CMAX): place them, sort each bucket by value, run the fine
+      // sweep; stores every pixel whose median lies in those buckets -- its
+      // walk ends in bucket b with residual rank R2 - #keys < b, and the median
+      // is that rank among b's in-window candidates in sorted order.
+      auto resolve = [&](const KeyFn<NB>& kf, int ba, int bb) {
+        const int base = start[ba];
+        for (int b = ba + lane; b <= bb; b += 32) cur[b] = start[b] - base;
         __syncwarp();
-        auto scan = [&](auto&& visit) {
-          uint32_t va[C::E], vb[C::E];
-          fetch_raw(0, va);
-          auto visit_all = [&](int q0, const uint32_t (&v)[C::E]) {
-#pragma unroll
-            for (int e = 0; e < C::E; e++)
-              if (valid(q0, e) && v[e] >= lo && v[e] <= hi) visit(v[e], pos_of(q0, e));
-          };
-          int q0 = 0;
-          for (; q0 + C::G < q_end; q0 += 2 * C::G) {
-            fetch_raw(q0 + C::G, vb);
-            visit_all(q0, va);
-            if (q0 + 2 * C::G < q_end) fetch_raw(q0 + 2 * C::G, va);
-            visit_all(q0 + C::G, vb);
-          }
-          if (q0 < q_end) visit_all(q0, va);
-        };
-        scan([&](uint32_t v, uint32_t) { lc[kf(v) * 32 + lane]++; });
-        __syncwarp();
-        // exclusive scan over (bucket, lane): bucket b of lane l starts at
-        // start[b] + sum of lanes < l; lane l walks the buckets in order
-        {
-          int run = 0;  // prefix over buckets (warp-uniform)
-          for (int b = 0; b < C::NB; b++) {
-            const int c = (int)lc[b * 32 + lane];
-            int incl = c;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-              const int y = __shfl_up_sync(0xffffffffu, incl, o);
-              if (lane >= o) incl += y;
-            }
-            lc[b * 32 + lane] = (uint32_t)(run + incl - c);  // this lane's cursor
-            if (lane == 0) start[b] = run;
-            run += __shfl_sync(0xffffffffu, incl, 31);
-          }
-          n_cand = run;
-          if (lane == 0) start[C::NB] = n_cand;
-        }
-        __syncwarp();
-        if (n_cand > C::CMAX) {
-          if (rows > 1) {  // too many candidates: halve the sub-item
-            Rcur = (rows + 1) / 2;
-            continue;
-          }
-          for (int c = 0; c < 2; c++)  // a single row that still does not fit
-            if (x + c < W)
-              dst[(int64_t)Y0 * job.dst_pitch + (int64_t)(x + c) * CH] =
-                  (T)brute_median<T, K>(src, job, job.out_y0 + Y0, x + c);
-          y0 += rows;
-          Rcur = rows_item;
-          continue;
-        }
-        RANK_T(1);
         scan([&](uint32_t v, uint32_t p) {
-          const int slot = (int)(lc[kf(v) * 32 + lane]++);
-          cval[slot] = (T)v;
-          cpos[slot] = (uint16_t)p;
+          const int b = kf(v);
+          if (b >= ba && b <= bb) {
+            const int slot = atomicAdd(&cur[b], 1);
+            cval[slot] = (T)v;
+            cpos[slot] = (uint16_t)p;
+          }
         });
         __syncwarp();
         RANK_T(2);
-        // sort each bucket by value: insertion sort per lane for small
-        // buckets, the whole warp (odd-even transposition) for large ones
-        for (int b = 1 + lane; b < C::NB - 1; b += 32) {
-          const int i0 = start[b], i1 = start[b + 1];
+        // small buckets: insertion sort, one bucket per lane
+        for (int b = ba + lane; b <= bb; b += 32) {
+          const int i0 = start[b] - base, i1 = start[b + 1] - base;
           if (i1 - i0 > 64) continue;
           for (int i = i0 + 1; i < i1; i++) {
             const T v = cval[i];
@@ -361,69 +350,258 @@ __global__ void __launch_bounds__(32) rank_kernel(Job job, int R, int n_strips, 
           }
         }
         __syncwarp();
-        for (int b = 1; b < C::NB - 1; b++) {
-          const int i0 = start[b], n = start[b + 1] - i0;
+        // large buckets: the warp's bitonic sort, all comparators ascending
+        // (mirror stage + half-cleaners), so indices >= n are never touched
+        for (int b = ba; b <= bb; b++) {
+          const int i0 = start[b] - base, n = start[b + 1] - start[b];
           if (n <= 64) continue;
-          for (int ph = 0; ph < n; ph++) {
-            for (int i = i0 + (ph & 1) + 2 * lane; i + 1 < i0 + n; i += 64) {
-              const T a = cval[i], c = cval[i + 1];
-              if (a > c) {
-                const uint16_t pa = cpos[i];
-                cval[i] = c;
-                cval[i + 1] = a;
-                cpos[i] = cpos[i + 1];
-                cpos[i + 1] = pa;
+          T* a = cval + i0;
+          uint16_t* ap = cpos + i0;
+          int N = 1;
+          while (N < n) N <<= 1;
+          auto cmpswap = [&](int lo_i, int hi_i) {
+            if (hi_i < n) {
+              const T x = a[lo_i], y = a[hi_i];
+              if (x > y) {
+                const uint16_t px = ap[lo_i];
+                a[lo_i] = y;
+                a[hi_i] = x;
+                ap[lo_i] = ap[hi_i];
+                ap[hi_i] = px;
               }
+            }
+          };
+          for (int kk = 2; kk <= N; kk <<= 1) {
+            const int hk = kk >> 1;
+            for (int i = lane; i < N / 2; i += 32) {
+              const int blk = (i / hk) * kk, o = i % hk;
+              cmpswap(blk + o, blk + kk - 1 - o);
             }
             __syncwarp();
+            for (int j = hk >> 1; j > 0; j >>= 1) {
+              for (int i = lane; i < N / 2; i += 32) {
+                const int l = 2 * j * (i / j) + (i % j);
+                cmpswap(l, l + j);
+              }
+              __syncwarp();
+            }
           }
+        }
+        __syncwarp();
+        RANK_T(3);
+        sweep(kf, [&](int t) {
+#pragma unroll
+          for (int c = 0; c < 2; c++) {
+            const int b = sw.m[c];
+            if (b >= ba && b <= bb) {
+              // r'-th in-window candidate of bucket b, in sorted order
+              int need = SW::R2 - sw.bl[c];
+              uint32_t v = 0;
+              const int cx = 2 * lane + c;  // window columns [cx, cx + K), rows [t, t + K)
+              // 4 candidates per round (independent loads), then the exact hit
+              const uint32_t pbase = ((uint32_t)t << 8) | (uint32_t)cx;
+              auto inwin = [&](uint32_t p) -> int {
+                const uint32_t d = p - pbase;  // column offset in bits 0..7 (row checked apart)
+                return (d & 0xFFu) < (uint32_t)K && ((p >> 8) - (uint32_t)t) < (uint32_t)K;
+              };
+              int i = start[b] - base;
+              const int i1 = start[b + 1] - base;
+              for (; i + 4 <= i1; i += 4) {
+                const int w0 = inwin(cpos[i]), w1 = inwin(cpos[i + 1]), w2 = inwin(cpos[i + 2]),
+                          w3 = inwin(cpos[i + 3]);
+                const int n4 = w0 + w1 + w2 + w3;
+                if (n4 >= need) {
+                  const int j = need <= w0 ? 0 : need <= w0 + w1 ? 1 : need <= w0 + w1 + w2 ? 2 : 3;
+                  v = cval[i + j];
+                  need = 0;
+                  break;
+                }
+                need -= n4;
+              }
+              for (; need > 0 && i < i1; i++)
+                if (inwin(cpos[i]) && --need == 0) v = cval[i];
+              put(t, c, v);
+            }
+          }
+        });
+      };
+
+#ifdef TMB_RANK_PROFILE
+      long long _t = clock64();
+#endif
+      int sp = 0;  // interval stack depth (warp-uniform); entries (lo, hi, bin width)
+      auto push = [&](uint32_t a, uint32_t b, uint32_t w) {
+        if (lane == 0) {
+          stk[3 * sp] = a;
+          stk[3 * sp + 1] = b;
+          stk[3 * sp + 2] = w;
+        }
+        sp++;
+        __syncwarp();
+      };
+      // ---- 0. guess the value range from every 8th footprint row -----------
+      uint32_t gmin = 0xFFFFFFFFu, gmax = 0u;
+      scan_rows(8, [&](uint32_t v, uint32_t) {
+        gmin = min(gmin, v);
+        gmax = max(gmax, v);
+      });
+      gmin = warp_min(gmin);
+      gmax = warp_max(gmax);
+      // ---- 1. first sweep over the guess; the stash measures the true range --
+      // keys are monotone in v, so a pixel's bin still brackets its median when
+      // samples fall outside the guess (they clamp to bins 0 / NB-1, whose
+      // value ranges end at the true footprint extremes)
+      if (gmax - gmin < kInner) {
+        // at most 126 values guessed: one value per bin -- pixels whose median
+        // lies inside are final; the clamped ends become intervals
+        const KeyFn<NB> kx{gmin, gmax, 0u, 0, 0};
+        int lo_any = 0, hi_any = 0;
+        sweep(kx, [&](int t) {
+#pragma unroll
+          for (int c = 0; c < 2; c++) {
+            const int bb = sw.m[c];
+            if (bb >= 1 && bb <= NB - 2) put(t, c, gmin + (uint32_t)(bb - 1));
+            if (x + c < W) {
+              lo_any |= bb == 0;
+              hi_any |= bb == NB - 1;
+            }
+          }
+        }, true);
+        fmin = warp_min(fmin);
+        fmax = warp_max(fmax);
+        if (__any_sync(0xffffffffu, lo_any) && fmin < gmin) push(fmin, gmin - 1, gmin - fmin);
+        if (__any_sync(0xffffffffu, hi_any) && fmax > gmax) push(gmax + 1, fmax, fmax - gmax);
+      } else {
+        const int s = 25 - __clz(gmax - gmin);  // bit length - 7 (>= 0: the range is >= 126)
+        int blo = NB - 1, bhi = 0;
+        sweep(KeyFn<NB>{gmin, gmax, 0u, -1, s}, [&](int) {
+          if (x < W) {
+            blo = min(blo, sw.m[0]);
+            bhi = max(bhi, sw.m[0]);
+          }
+          if (x + 1 < W) {
+            blo = min(blo, sw.m[1]);
+            bhi = max(bhi, sw.m[1]);
+          }
+        }, true);
+        blo = (int)warp_min((uint32_t)blo);
+        bhi = (int)warp_max((uint32_t)bhi);
+        fmin = warp_min(fmin);
+        fmax = warp_max(fmax);
+        const uint32_t lo = blo == 0 ? fmin : gmin + ((uint32_t)blo << s);
+        const uint32_t hi = bhi == NB - 1
+                                ? fmax
+                                : (uint32_t)min((uint64_t)fmax, (uint64_t)gmin + (((uint64_t)bhi + 1) << s) - 1);
+        push(max(lo, fmin), hi, 1u << s);
+      }
+      RANK_T(0);
+      // ---- 2. resolve every interval that may hold medians ------------------
+      while (sp > 0) {
+        sp--;
+        uint32_t lo = stk[3 * sp], hi = stk[3 * sp + 1];
+        const uint32_t wprev = stk[3 * sp + 2];  // width of the bins that produced it
+        __syncwarp();
+        const uint64_t span = (uint64_t)(hi - lo) + 1;
+        if (span <= kInner) {
+          slice(lo, hi);
+          continue;
+        }
+        // count scan: candidates (samples in [lo, hi]) per fine bucket with
+        // lane-private counters in the (idle) histogram words -- counter
+        // (bucket, lane) at word bucket * 32 + lane, no contention -- plus
+        // their exact value range
+        const uint32_t mul = (uint32_t)(((uint64_t)kInner << 32) / span);
+        const KeyFn<NB> kf{lo, hi, mul, 1, 0};
+        uint32_t* lc = smem;
+        for (int b = 0; b < NB; b++) lc[b * 32 + lane] = 0;
+        __syncwarp();
+        uint32_t tmin = 0xFFFFFFFFu, tmax = 0u;
+        scan([&](uint32_t v, uint32_t) {
+          if (v >= lo && v <= hi) {
+            lc[kf(v) * 32 + lane]++;
+            tmin = min(tmin, v);
+            tmax = max(tmax, v);
+          }
+        });
+        __syncwarp();
+        int n_cand;
+        {
+          int run = 0;  // bucket offsets start[b]: prefix over buckets (warp-uniform)
+          for (int b0 = 0; b0 < NB; b0 += 32) {
+            uint32_t c = 0;  // bucket b0 + lane, summed over the lanes' counters
+#pragma unroll 8
+            for (int l = 0; l < 32; l++) c += lc[(b0 + lane) * 32 + ((l + lane) & 31)];
+            int incl = (int)c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const int y = __shfl_up_sync(0xffffffffu, incl, o);
+              if (lane >= o) incl += y;
+            }
+            start[b0 + lane] = run + incl - (int)c;
+            run += __shfl_sync(0xffffffffu, incl, 31);
+          }
+          n_cand = run;
+          if (lane == 0) start[NB] = n_cand;
+        }
+        __syncwarp();
+        RANK_T(1);
+        if (n_cand == 0) continue;
+        if (n_cand <= C::CMAX) {
+          resolve(kf, 1, NB - 2);
+          continue;
+        }
+        // too many candidates: the medians are spread (gradients, smooth
+        // fields, impulse noise over them)
+        lo = warp_min(tmin);
+        hi = warp_max(tmax);
+        const uint64_t span2 = (uint64_t)(hi - lo) + 1;
+        const uint64_t wnew = (span2 + kInner - 1) / kInner;  // bucket width over [lo, hi]
+        const int nsl = (int)min((uint64_t)1 << 20, wnew);     // exact slices to cover it
+        const int ngr = (n_cand + (C::CMAX * 3 / 4) - 1) / (C::CMAX * 3 / 4);
+        if (nsl <= 2 || nsl <= ngr) {  // few values: exact slices
+          slices(lo, hi);
+          continue;
+        }
+        if ((uint64_t)wprev >= 4 * wnew && sp < kStack) {
+          // the candidates reach far beyond the medians (outliers, gaps):
+          // an interval sweep of 126 buckets over [lo, hi], then the samples
+          // of the buckets holding medians give the next interval
+          const KeyFn<NB> km{lo, hi, (uint32_t)(((uint64_t)kInner << 32) / span2), 1, 0};
+          int b0, b1;
+          range_pass(km, b0, b1);
+          uint32_t t0 = 0xFFFFFFFFu, t1 = 0u;
+          scan([&](uint32_t v, uint32_t) {
+            const int kb = km(v);
+            if (kb >= b0 && kb <= b1) {
+              t0 = min(t0, v);
+              t1 = max(t1, v);
+            }
+          });
+          push(warp_min(t0), warp_max(t1), (uint32_t)wnew);
+          continue;
+        }
+        // dense spread candidates: groups of consecutive buckets that fit,
+        // one fine sweep each
+        for (int b = 1; b <= NB - 2;) {
+          const int cb = start[b + 1] - start[b];
+          if (cb > C::CMAX) {
+            // one bucket alone does not fit: its exact value range becomes an
+            // interval of its own (126 finer buckets), or slices if the stack is full
+            const uint32_t v0 = kf.first_of(b), v1 = kf.first_of(b + 1) - 1;
+            if (sp < kStack)
+              push(v0, v1, (uint32_t)min((uint64_t)0xFFFFFFFFu, (span + kInner - 1) / kInner));
+            else
+              slices(v0, v1);
+            b++;
+            continue;
+          }
+          int e = b;
+          while (e + 1 <= NB - 2 && start[e + 2] - start[b] <= C::CMAX) e++;
+          if (start[e + 1] > start[b]) resolve(kf, b, e);
+          b = e + 1;
         }
       }
-
-      RANK_T(3);
-      // ---- 3. fine pass -----------------------------------------------------
-      sweep(sw, kf, [&](int t) {
-#pragma unroll
-        for (int c = 0; c < 2; c++) {
-          const int b = sw.m[c];
-          uint32_t v = 0;
-          if (b < 1 || b > C::NB - 2) {
-            // only columns beyond the image edge (excluded from [lo, hi]) land here
-          } else if (f == 0) {
-            v = lo + (uint32_t)(b - 1);
-          } else {
-            // r'-th in-window candidate of bin b, in sorted order
-            int need = SW::R2 - sw.bl[c];
-            const int cx = 2 * lane + c;  // window columns [cx, cx + K), rows [t, t + K)
-            // 4 candidates per round (independent loads), then the exact hit
-            const uint32_t base = ((uint32_t)t << 8) | (uint32_t)cx;
-            auto inwin = [&](uint32_t p) -> int {
-              const uint32_t d = p - base;  // column offset in bits 0..7 (row checked apart)
-              return (d & 0xFFu) < (uint32_t)K && ((p >> 8) - (uint32_t)t) < (uint32_t)K;
-            };
-            int i = start[b];
-            const int i1 = start[b + 1];
-            for (; i + 4 <= i1; i += 4) {
-              const int w0 = inwin(cpos[i]), w1 = inwin(cpos[i + 1]), w2 = inwin(cpos[i + 2]),
-                        w3 = inwin(cpos[i + 3]);
-              const int n4 = w0 + w1 + w2 + w3;
-              if (n4 >= need) {
-                const int j = need <= w0 ? 0 : need <= w0 + w1 ? 1 : need <= w0 + w1 + w2 ? 2 : 3;
-                v = cval[i + j];
-                need = 0;
-                break;
-              }
-              need -= n4;
-            }
-            for (; need > 0 && i < i1; i++)
-              if (inwin(cpos[i]) && --need == 0) v = cval[i];
-          }
-          if (x + c < W) dst[(int64_t)(Y0 + t) * job.dst_pitch + (int64_t)(x + c) * CH] = (T)v;
-        }
-      });
       RANK_T(4);
-      y0 += rows;
-      Rcur = rows_item;
     }
   }
 }
@@ -434,7 +612,8 @@ int launch_rank_k(const Job& job, cudaStream_t stream) {
   constexpr int kSmem = C::kWarpBytes;
   static_assert(kSmem <= 227 * 1024, "rank kernel does not fit in shared memory");
   auto fn = rank_kernel<T, K>;
-  static const LaunchInfo li = launch_info(fn, 32, kSmem);
+  static LaunchCache cache;
+  const LaunchInfo li = cache.get(fn, 32, kSmem);
   if (li.err != cudaSuccess) return (int)li.err;
   const int sms = li.sms, occ = li.occ;
   const int n_strips = (job.width + 63) / 64;

@@ -82,7 +82,30 @@ def _bits_of(dtype) -> int:
             "and uint32 images (no CPU fallback)") from None
 
 
-def _run_numpy(img: np.ndarray, kw: int, kh: int, variant: str, device: int) -> np.ndarray:
+def pinned_empty(shape, dtype) -> np.ndarray:
+    """A numpy array in pinned (page-locked) host memory from the C ABI's cache.
+
+    The drop-in returns its numpy outputs in these, so the device-to-host copy
+    runs at full PCIe speed; the block goes back to the cache when the array
+    (and every view of it) is garbage collected.
+    """
+    import ctypes
+    import weakref
+
+    dtype = np.dtype(dtype)
+    n = max(1, int(np.prod(shape, dtype=np.int64)) * dtype.itemsize)
+    lib = _lib.load()
+    ptr = lib.tm_host_alloc(n)
+    if not ptr:  # pinned memory exhausted: a pageable output (the copy stages it)
+        return np.empty(shape, dtype)
+    buf = (ctypes.c_uint8 * n).from_address(ptr)
+    weakref.finalize(buf, lib.tm_host_free, ptr)
+    count = int(np.prod(shape, dtype=np.int64))
+    return np.frombuffer(buf, dtype=dtype, count=count).reshape(shape)
+
+
+def _run_numpy(img: np.ndarray, kw: int, kh: int, variant: str, device: int,
+               devices=None) -> np.ndarray:
     bits = _bits_of(img.dtype)
     if img.ndim == 2:
         h, w = img.shape
@@ -94,24 +117,36 @@ def _run_numpy(img: np.ndarray, kw: int, kh: int, variant: str, device: int) -> 
         src.ndim == 2 or src.strides[1] == ch * src.itemsize)
     if not rows_ok:
         src = np.ascontiguousarray(src)
-    out = np.empty((h, w) if ch == 1 else (h, w, ch), dtype=img.dtype)
+    out = pinned_empty(img.shape, img.dtype)
     lib = _lib.load()
-    rc = lib.tm_median2d_host(src.ctypes.data, src.strides[0], out.ctypes.data, out.strides[0],
-                              w, h, ch, bits, kw, kh, _lib.VARIANT_CODES[variant], device)
+    code = _lib.VARIANT_CODES[variant]
+    if devices is not None and len(devices) > 1:
+        import ctypes
+        ids = (ctypes.c_int32 * len(devices))(*[int(d) for d in devices])
+        rc = lib.tm_median2d_host_multi(src.ctypes.data, src.strides[0], out.ctypes.data,
+                                        out.strides[0], w, h, ch, bits, kw, kh, code, ids,
+                                        len(devices))
+    else:
+        dev = int(devices[0]) if devices else device
+        rc = lib.tm_median2d_host(src.ctypes.data, src.strides[0], out.ctypes.data,
+                                  out.strides[0], w, h, ch, bits, kw, kh, code, dev)
     _lib.check(rc)
     return out
 
 
-def _run_torch(img, kw: int, kh: int, variant: str):
+def _run_torch(img, kw: int, kh: int, variant: str, devices=None):
     import torch
 
     dt = {torch.uint8: 8, torch.uint16: 16, torch.uint32: 32}.get(img.dtype)
     if dt is None:
         raise TypeError(f"unsupported element type {img.dtype}: expected uint8/16/32")
     if not img.is_cuda:
-        out = _run_numpy(img.numpy(), kw, kh, variant, 0)
+        out = _run_numpy(img.numpy(), kw, kh, variant, 0, devices)
         return torch.from_numpy(out)
     src = img.contiguous()
+    if devices is not None and len(devices) > 1:
+        from .bands import filter_sharded
+        return filter_sharded(src, kw, kh, variant, devices)
     out = torch.empty_like(src)
     if src.ndim == 2:
         h, w = src.shape
@@ -134,12 +169,15 @@ def _empty_oracle_error(shape) -> ValueError:
 
 
 def filter_image(image, k, variant="auto", *, root=None, workers=1, slice_budget=None,
-                 counter=None, checksums=None, device: int = 0):
+                 counter=None, checksums=None, device: int = 0, devices=None):
     """Median-filter ``image`` exactly, edge-replicated borders (engine.py:29-52).
 
     ``k`` is an odd kernel diameter or a KernelSpec (rectangular kernels take
     the oblivious route, as in the reference).  ``device`` selects the GPU for
-    numpy inputs (torch tensors run on their own device).
+    numpy inputs (torch tensors run on their own device).  ``devices`` (a list
+    of GPU ordinals) shards the image into one row band per GPU with a
+    k/2-row halo each -- bit-identical to one GPU; torch inputs come back on
+    their own device.
     """
     if variant not in VARIANTS:
         raise ValueError(f"unknown variant {variant!r} (expected one of {VARIANTS})")
@@ -176,8 +214,8 @@ def filter_image(image, k, variant="auto", *, root=None, workers=1, slice_budget
             raise ValueError("expected a 2-D image")
         if 0 in shape:
             raise ValueError(f"image dims must be positive, got {shape[1]}x{shape[0]}")
-    out = (_run_torch(img, kern.k_w, kern.k_h, launch) if torch_in
-           else _run_numpy(img, kern.k_w, kern.k_h, launch, device))
+    out = (_run_torch(img, kern.k_w, kern.k_h, launch, devices) if torch_in
+           else _run_numpy(img, kern.k_w, kern.k_h, launch, device, devices))
     if variant == "aware" and (counter is not None or checksums is not None):
         H, W = shape
         itemsize = img.element_size() if torch_in else img.itemsize
@@ -216,15 +254,19 @@ def filter_planes(image, k, variant="auto", **kwargs):
             return torch.stack(planes, dim=-1)
         return np.stack(planes, axis=-1)
     h, w, ch = (int(s) for s in img.shape)
-    if ch == 0 or h == 0 or w == 0:
-        return img[...] if torch_in else np.empty_like(img)
+    if ch == 0:  # the reference stacks zero planes (engine.py:63)
+        raise ValueError("need at least one array to stack")
+    if h == 0 or w == 0:  # the reference filters plane 0 first, which raises
+        return filter_image(img[..., 0], k, variant, **kwargs)
     v = pick_variant(k) if variant == "auto" else variant
     # validate exactly as filter_image would for one plane
     probe = np.empty((1, 1), dtype=np.uint8)
     _validate_like_plane(probe, k, v, kwargs.get("root"))
     kern = as_kernel(k)
-    return (_run_torch(img, kern.k_w, kern.k_h, variant) if torch_in
-            else _run_numpy(img, kern.k_w, kern.k_h, variant, int(kwargs.get("device", 0))))
+    devices = kwargs.get("devices")
+    return (_run_torch(img, kern.k_w, kern.k_h, variant, devices) if torch_in
+            else _run_numpy(img, kern.k_w, kern.k_h, variant, int(kwargs.get("device", 0)),
+                            devices))
 
 
 def _validate_like_plane(probe, k, variant, root) -> None:

@@ -2,12 +2,8 @@
 
     python tools/patterns.py --size 4096 --bits 16 --k 27 49 75 --patterns random gradient impulse constant
 
-Patterns follow the reference generator (reference.py:78-99): constant
-(1 << (bits-1)), gradient ((x + y) & max), impulse (gradient with 30 % salt /
-pepper), random (uniform over the dtype), plus ``narrow16`` (uniform in
-[0, 65535] stored in a wider dtype) and ``smooth`` (a smooth field plus
-Gaussian noise, sigma 200).  Images are generated on the device with a seeded
-torch generator.  Timing: CUDA events on the launching stream, L2 flushed
+Patterns: paper_2507_19926_b200.synth (the reference generator's patterns plus
+narrow16 / gentle / smooth), rendered on the device with a seeded generator.  Timing: CUDA events on the launching stream, L2 flushed
 (256 MiB write) before every rep, median of --reps; SM clocks sampled via NVML.
 Optional --check compares a few random rows against the C oracle (banded).
 """
@@ -22,37 +18,13 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2507_19926_b200 import _lib  # noqa: E402
+from paper_2507_19926_b200.synth import render  # noqa: E402
 
 TDT = {8: torch.uint8, 16: torch.uint16, 32: torch.uint32}
 
 
 def make(pattern: str, h: int, w: int, bits: int, seed: int = 42) -> torch.Tensor:
-    dev = "cuda"
-    mx = (1 << bits) - 1
-    g = torch.Generator(device=dev).manual_seed(seed)
-    ys = torch.arange(h, device=dev, dtype=torch.int64)[:, None]
-    xs = torch.arange(w, device=dev, dtype=torch.int64)[None, :]
-    if pattern == "constant":
-        t = torch.full((h, w), 1 << (bits - 1), device=dev, dtype=torch.int64)
-    elif pattern == "gradient":
-        t = (xs + ys) & mx
-    elif pattern == "random":
-        t = torch.randint(0, mx + 1, (h, w), generator=g, device=dev, dtype=torch.int64)
-    elif pattern == "narrow16":
-        t = torch.randint(0, 1 << 16, (h, w), generator=g, device=dev, dtype=torch.int64)
-    elif pattern == "impulse":
-        t = (xs + ys) & mx
-        hit = torch.rand((h, w), generator=g, device=dev) < 0.3
-        salt = torch.rand((h, w), generator=g, device=dev) < 0.5
-        t = torch.where(hit & salt, torch.full_like(t, mx), t)
-        t = torch.where(hit & ~salt, torch.zeros_like(t), t)
-    elif pattern == "smooth":
-        base = (torch.sin(xs / 517.0) * torch.cos(ys / 311.0) + 1.0) * 0.45 * mx
-        noise = torch.randn((h, w), generator=g, device=dev) * 200.0
-        t = (base + noise + 0.05 * mx).clamp(0, mx).to(torch.int64)
-    else:
-        raise ValueError(pattern)
-    return t.to(TDT[bits])
+    return render(pattern, (h, w), bits, seed)
 
 
 def main():
