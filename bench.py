@@ -130,6 +130,11 @@ class ClockSampler:
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
+        # the first sample lands before the timed region starts (NVML init
+        # takes longer than a short timed region)
+        t0 = time.time()
+        while not self.samples and self._t.is_alive() and time.time() - t0 < 5.0:
+            time.sleep(0.001)
         return self
 
     def __exit__(self, *exc):

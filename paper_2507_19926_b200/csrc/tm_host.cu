@@ -77,12 +77,12 @@ class CopyPool {
     done_cv_.wait(g, [&] { return job.done == job.n && job.users == 0; });
     cur_ = nullptr;
   }
-  // Row copy of `rows` rows of `row_bytes`, parallel over ~4 MB pieces.
+  // Row copy of `rows` rows of `row_bytes`, parallel over pieces of >= 256 KB.
   void copy2d(char* dst, int64_t dpitch, const char* src, int64_t spitch, int64_t row_bytes,
               int64_t rows) {
     if (rows <= 0) return;
     const int64_t total = row_bytes * rows;
-    const int pieces = (int)std::max<int64_t>(1, std::min<int64_t>(4 * size(), total >> 22));
+    const int pieces = (int)std::max<int64_t>(1, std::min<int64_t>(2 * size(), total >> 18));
     const bool flat = dpitch == row_bytes && spitch == row_bytes;
     run(pieces, [&](int i) {
       if (flat) {

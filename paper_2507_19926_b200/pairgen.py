@@ -64,7 +64,8 @@ def emit_pair_program(k: int, tw: int, th: int, name: str) -> tuple[str, dict]:
     half = Program(kern, dims)
     xs = list(root.core_xs())[:hw]
     flat = [half.col(x, i) for x in xs for i in range(root.core_h)]
-    hvals = half.run(nets.multiway_merge((root.core_h,) * hw), flat)
+    hvals = half.run(nets.multiway_merge((root.core_h,) * hw), flat, ("core-half", 0),
+                     runs=(root.core_h,) * hw)
     half.outputs = [hvals]
     names: dict = {}
 
@@ -87,7 +88,7 @@ def emit_pair_program(k: int, tw: int, th: int, name: str) -> tuple[str, dict]:
     fin = Program(kern, dims)
     a_ids = [fin.pix(0, i) for i in range(n)]      # placeholders: own half
     b_ids = [fin.pix(1, i) for i in range(n)]      # placeholders: other half
-    merged = fin.run(nets.oddeven_merge(n, n), a_ids + b_ids)
+    merged = fin.run(nets.oddeven_merge(n, n), a_ids + b_ids, ("core-pair", 0), runs=(n, n))
     win = retention_window(kern.count, root.core_w * root.core_h)
     cand_ids = merged[win.lo - 1: win.hi]
     fin.outputs = [cand_ids]
@@ -110,7 +111,7 @@ def emit_pair_program(k: int, tw: int, th: int, name: str) -> tuple[str, dict]:
     row_ids = {}
     for y in top:
         row_ids[y] = rows_prog.run(nets.make_sorter(root.core_w),
-                                   [rows_prog.pix(x, y) for x in root.core_xs()])
+                                   [rows_prog.pix(x, y) for x in root.core_xs()], ("rowsort", 0))
     rows_prog.outputs = [[v for y in top for v in row_ids[y]]]
     rnames: dict = {}
 

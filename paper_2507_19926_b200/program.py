@@ -35,6 +35,7 @@ from .geometry import (KernelSpec, Region, TileDims, as_kernel, region,
                        retention_window, root_tile_size, split)
 
 MAX_TILE_AREA = 256       # reference oblivious.py:49
+RECORD = None             # netexport: list collecting every network application
 DRIVER_ROOT_CAP = 16      # reference oblivious.py:50
 
 
@@ -75,11 +76,16 @@ class Program:
     def col(self, x: int, i: int) -> int:
         return self._mk(("col", x, i))
 
-    def run(self, net, wires: list[int], label=None) -> list[int]:
+    def run(self, net, wires: list[int], label=None, runs=None) -> list[int]:
+        """Apply network ``net`` to ``wires``; ``runs`` = the sorted input runs
+        of a merge (None for a sort) -- what the stage claims, for netexport."""
         w = list(wires)
         lab = label or self._label
         st = self.n_stages
         self.n_stages += 1
+        if RECORD is not None:
+            RECORD.append((self, lab, tuple(net), None if runs is None else tuple(runs),
+                           tuple(wires)))
         for i, j in net:
             a, b = w[i], w[j]
             w[i] = self._mk(("min", a, b))
@@ -266,7 +272,8 @@ def build_program(k, tile=None, cse: bool = True, remat: bool = False,
     seen = root.core_w * root.core_h
     win = retention_window(n_total, seen)
     flat = [v for x in root.core_xs() for v in col_runs[x][0]]
-    merged = prog.run(nets.multiway_merge((root.core_h,) * root.core_w), flat, ("core", 0))
+    merged = prog.run(nets.multiway_merge((root.core_h,) * root.core_w), flat, ("core", 0),
+                      runs=(root.core_h,) * root.core_w)
     cand = merged[win.lo - 1: win.hi]
     prog.root_cand = list(cand)
     prog.root_rows = {y: list(r[0]) for y, r in row_runs.items()}
@@ -289,7 +296,7 @@ def build_program(k, tile=None, cse: bool = True, remat: bool = False,
             else:
                 sizes = tuple(len(r) for r in runs)
                 pack = prog.run(nets.multiway_merge(sizes), [v for r in runs for v in r],
-                                ("pack", dep))
+                                ("pack", dep), runs=sizes)
             seen2 = seen + len(pack)
             w = retention_window(n_total, seen2)
             lo, hi = w.lo - 1 - d_lo, w.hi - 1 - d_lo
@@ -303,7 +310,8 @@ def build_program(k, tile=None, cse: bool = True, remat: bool = False,
                 ca = ca[lo_a: hi + 1]
                 pa = pa[lo_b: hi + 1]
                 lo, hi = lo - lo_a - lo_b, hi - lo_a - lo_b
-            both = prog.run(nets.oddeven_merge(len(ca), len(pa)), ca + pa, ("cand", dep))
+            both = prog.run(nets.oddeven_merge(len(ca), len(pa)), ca + pa, ("cand", dep),
+                            runs=(len(ca), len(pa)))
             cand_stages.append(prog.n_stages - 1)
             if len(cand_stages) == 2:
                 prog.companions[cand_stages[0]] = [cand_stages[1]]
@@ -323,7 +331,7 @@ def build_program(k, tile=None, cse: bool = True, remat: bool = False,
                     if len(add) > 1:
                         add = prog.run(nets.make_sorter(len(add)), add, ("cornersort", dep))
                     vals = prog.run(nets.oddeven_merge(len(base), len(add)), base + add,
-                                    ("extend", dep))
+                                    ("extend", dep), runs=(len(base), len(add)))
                 grown[key] = (vals, allcells, True)
             if axis == "h":
                 kcols = {x: cols[x] for x in kid.region.extra_xs()}
