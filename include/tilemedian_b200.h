@@ -14,6 +14,8 @@
  *   tm_median2d_host_multi <- filter_image(..., devices=[...]): one row band
  *                         per GPU, each re-reading its k_h/2 halo rows (the
  *                         reference's banding, aware.py:455-491)
+ *   tm_median2d_host_frames <- a batch of frames (filter_frames): frames split
+ *                         across the GPUs, no communication
  *   tm_median2d_bands  <- the same banding on device-resident bands: halo rows
  *                         exchanged between the GPUs (peer copies over NVLink)
  *   tm_host_alloc/free <- the reference returns a fresh host array
@@ -95,6 +97,16 @@ int tm_median2d_host(const void* src, int64_t src_pitch, void* dst, int64_t dst_
                      int32_t width, int32_t height, int32_t channels, int32_t bits,
                      int32_t k_w, int32_t k_h, int32_t variant, int32_t device);
 
+/* tm_median2d_host with the device memory held per call bounded by
+ * device_budget bytes (0 = half the free memory): the image is processed in
+ * row bands whose buffers (source rows with their k_h/2 halos + output rows)
+ * fit (at least one output row per band) -- the reference's slice_budget
+ * banding (aware.py:455-463); the result does not depend on the budget. */
+int tm_median2d_host_budget(const void* src, int64_t src_pitch, void* dst, int64_t dst_pitch,
+                            int32_t width, int32_t height, int32_t channels, int32_t bits,
+                            int32_t k_w, int32_t k_h, int32_t variant, int32_t device,
+                            int64_t device_budget);
+
 /* Host buffers split into n_dev balanced row bands, one per device in
  * dev_ids, filtered concurrently (a repeated ordinal runs its bands one after
  * the other); every device copies its
@@ -104,6 +116,16 @@ int tm_median2d_host_multi(const void* src, int64_t src_pitch, void* dst, int64_
                            int32_t width, int32_t height, int32_t channels, int32_t bits,
                            int32_t k_w, int32_t k_h, int32_t variant, const int32_t* dev_ids,
                            int32_t n_dev);
+
+/* A batch of n_frames independent host images (frame f at src + f *
+ * src_frame_bytes, output at dst + f * dst_frame_bytes), frame f filtered on
+ * device dev_ids[f % n_dev]; devices run concurrently, no communication.
+ * Synchronises. */
+int tm_median2d_host_frames(const void* src, int64_t src_pitch, int64_t src_frame_bytes,
+                            void* dst, int64_t dst_pitch, int64_t dst_frame_bytes,
+                            int32_t n_frames, int32_t width, int32_t height, int32_t channels,
+                            int32_t bits, int32_t k_w, int32_t k_h, int32_t variant,
+                            const int32_t* dev_ids, int32_t n_dev);
 
 /* Device-resident row bands of one image, band i (rows top to bottom) on
  * device dev_ids[i].  band_buf[i] holds h = k_h/2 halo rows, then its

@@ -6,7 +6,7 @@ same signature, variants, validation and replicate borders, bit-exact output,
 computed by hand-written CUDA kernels behind a C ABI
 (``include/tilemedian_b200.h``).  See DESIGN.md.
 """
-from .engine import (AUTO_CROSSOVER, VARIANTS, dispatch_query, filter_image,
+from .engine import (AUTO_CROSSOVER, VARIANTS, dispatch_query, filter_frames, filter_image,
                      filter_planes, pick_variant)
 from .geometry import KernelSpec, TileDims, retention_window, root_tile_size
 from .model import ComparisonCounter, comparison_count
@@ -15,7 +15,7 @@ from .program import build_program, op_model
 __version__ = "0.1.0"
 
 __all__ = [
-    "AUTO_CROSSOVER", "VARIANTS", "filter_image", "filter_planes", "pick_variant",
+    "AUTO_CROSSOVER", "VARIANTS", "filter_image", "filter_planes", "filter_frames", "pick_variant",
     "dispatch_query", "KernelSpec", "TileDims", "retention_window", "root_tile_size",
     "ComparisonCounter", "comparison_count", "build_program", "op_model", "__version__",
 ]

@@ -33,8 +33,13 @@ _SIGS = {
                                         c_i32, c_i32, c_i32, c_i32, c_vp]),
     "tm_median2d_host": (ctypes.c_int, [c_vp, c_i64, c_vp, c_i64, c_i32, c_i32, c_i32, c_i32, c_i32,
                                         c_i32, c_i32, c_i32]),
+    "tm_median2d_host_budget": (ctypes.c_int, [c_vp, c_i64, c_vp, c_i64, c_i32, c_i32, c_i32, c_i32,
+                                               c_i32, c_i32, c_i32, c_i32, c_i64]),
     "tm_median2d_host_multi": (ctypes.c_int, [c_vp, c_i64, c_vp, c_i64, c_i32, c_i32, c_i32, c_i32,
                                               c_i32, c_i32, c_i32, c_vp, c_i32]),
+    "tm_median2d_host_frames": (ctypes.c_int, [c_vp, c_i64, c_i64, c_vp, c_i64, c_i64, c_i32, c_i32,
+                                               c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_vp,
+                                               c_i32]),
     "tm_median2d_bands": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32,
                                          c_i32, c_i32, c_i32, c_i32, c_vp]),
     "tm_host_alloc": (c_vp, [c_i64]),

@@ -302,7 +302,7 @@ struct HostArgs {
 // and D2H copies run concurrently (PCIe is full duplex).  A pageable source is
 // staged into pinned memory by the copy workers a chunk ahead of its DMA; a
 // pageable destination is drained from pinned memory as each D2H lands.
-int host_range(const HostArgs& a, int device, int ya, int yb) {
+int host_chunk(const HostArgs& a, int device, int ya, int yb) {
   if (device < 0 || device >= kMaxDev) return set_error(TM_EINVAL, "bad device %d", device);
   DevRes& r = g_dev[device];
   std::lock_guard<std::mutex> lock(r.mu);
@@ -415,6 +415,36 @@ int host_range(const HostArgs& a, int device, int ya, int yb) {
   return TM_OK;
 }
 
+// Output rows [ya, yb) on `device` in memory bands: each band's device
+// buffers (its source rows with the k_h/2 halos + its output rows) stay within
+// `budget` bytes (0 = half of the device's free memory) -- the reference's
+// slice_budget banding (aware.py:455-463), exact for the same reason: every
+// band re-reads its halo rows from the original image.
+int host_range(const HostArgs& a, int device, int ya, int yb, int64_t budget = 0) {
+  const int64_t row = (int64_t)a.width * a.channels * (a.bits / 8);
+  const int halo = a.k_h / 2;
+  if (budget <= 0) {
+    size_t fr = 0, tot = 0;
+    int prev = -1;
+    cudaGetDevice(&prev);
+    if (cudaSetDevice(device) == cudaSuccess && cudaMemGetInfo(&fr, &tot) == cudaSuccess)
+      budget = (int64_t)(fr / 2) + (int64_t)g_dev[device < kMaxDev && device >= 0 ? device : 0].dbytes;
+    else
+      cudaGetLastError();
+    if (prev >= 0) cudaSetDevice(prev);
+    if (budget <= 0) budget = (int64_t)1 << 30;
+  }
+  const int64_t per = budget / row;  // rows that fit
+  // a budget below one output row plus its halos still works, one row per band
+  // (like the reference, whose bands shrink to one tile row)
+  const int64_t chunk = std::max<int64_t>(1, (per - 2 * halo) / 2);
+  for (int y = ya; y < yb; y += (int)std::min<int64_t>(chunk, yb - y)) {
+    const int rc = host_chunk(a, device, y, (int)std::min<int64_t>(yb, y + chunk));
+    if (rc) return rc;
+  }
+  return TM_OK;
+}
+
 int check_host(const HostArgs& a) {
   if (a.bits != 8 && a.bits != 16 && a.bits != 32)
     return set_error(TM_ETYPE, "unsupported element width %d bits (expected 8, 16 or 32)", a.bits);
@@ -438,12 +468,21 @@ extern "C" {
 int tm_median2d_host(const void* src, int64_t src_pitch, void* dst, int64_t dst_pitch,
                      int32_t width, int32_t height, int32_t channels, int32_t bits, int32_t k_w,
                      int32_t k_h, int32_t variant, int32_t device) {
+  return tm_median2d_host_budget(src, src_pitch, dst, dst_pitch, width, height, channels, bits,
+                                 k_w, k_h, variant, device, 0);
+}
+
+int tm_median2d_host_budget(const void* src, int64_t src_pitch, void* dst, int64_t dst_pitch,
+                            int32_t width, int32_t height, int32_t channels, int32_t bits,
+                            int32_t k_w, int32_t k_h, int32_t variant, int32_t device,
+                            int64_t device_budget) {
   const HostArgs a{static_cast<const char*>(src), src_pitch, static_cast<char*>(dst), dst_pitch,
                    width, height, channels, bits, k_w, k_h, variant};
   int rc = check_host(a);
   if (rc) return rc;
+  if (device < 0 || device >= kMaxDev) return set_error(TM_EINVAL, "bad device %d", device);
   DeviceGuard guard;
-  return host_range(a, device, 0, height);
+  return host_range(a, device, 0, height, device_budget);
 }
 
 int tm_median2d_host_multi(const void* src, int64_t src_pitch, void* dst, int64_t dst_pitch,
@@ -472,6 +511,52 @@ int tm_median2d_host_multi(const void* src, int64_t src_pitch, void* dst, int64_
     });
   }
   for (auto& t : th) t.join();
+  for (int i = 0; i < n; i++)
+    if (rcs[i]) return set_error(rcs[i], "device %d: %s", dev_ids[i], errs[i].c_str());
+  return TM_OK;
+}
+
+int tm_median2d_host_frames(const void* src, int64_t src_pitch, int64_t src_frame_bytes,
+                            void* dst, int64_t dst_pitch, int64_t dst_frame_bytes,
+                            int32_t n_frames, int32_t width, int32_t height, int32_t channels,
+                            int32_t bits, int32_t k_w, int32_t k_h, int32_t variant,
+                            const int32_t* dev_ids, int32_t n_dev) {
+  if (n_frames < 0) return set_error(TM_EINVAL, "bad frame count %d", n_frames);
+  if (n_frames == 0) return TM_OK;
+  const HostArgs a0{static_cast<const char*>(src), src_pitch, static_cast<char*>(dst), dst_pitch,
+                    width, height, channels, bits, k_w, k_h, variant};
+  int rc = check_host(a0);
+  if (rc) return rc;
+  const int64_t frame = (int64_t)height * std::max(src_pitch, dst_pitch);
+  if (src_frame_bytes < (int64_t)height * src_pitch || dst_frame_bytes < (int64_t)height * dst_pitch)
+    return set_error(TM_EINVAL, "frame stride smaller than a frame (%lld bytes)", (long long)frame);
+  if (n_dev < 1 || !dev_ids) return set_error(TM_EINVAL, "need at least one device");
+  DeviceGuard guard;
+  // frames are independent: frame f goes to device dev_ids[f % n_dev], one
+  // host thread per device, no communication ("batches of frames are split
+  // across GPUs")
+  const int n = std::min(n_dev, n_frames);
+  std::vector<int> rcs(n, TM_OK);
+  std::vector<std::string> errs(n);
+  auto work = [&](int i) {
+    for (int f = i; f < n_frames; f += n) {
+      HostArgs a = a0;
+      a.src += (int64_t)f * src_frame_bytes;
+      a.dst += (int64_t)f * dst_frame_bytes;
+      rcs[i] = host_range(a, dev_ids[i], 0, height);
+      if (rcs[i]) {
+        errs[i] = tm_last_error();
+        return;
+      }
+    }
+  };
+  if (n == 1) {
+    work(0);
+  } else {
+    std::vector<std::thread> th;
+    for (int i = 0; i < n; i++) th.emplace_back(work, i);
+    for (auto& t : th) t.join();
+  }
   for (int i = 0; i < n; i++)
     if (rcs[i]) return set_error(rcs[i], "device %d: %s", dev_ids[i], errs[i].c_str());
   return TM_OK;

@@ -105,7 +105,11 @@ def pinned_empty(shape, dtype) -> np.ndarray:
 
 
 def _run_numpy(img: np.ndarray, kw: int, kh: int, variant: str, device: int,
-               devices=None) -> np.ndarray:
+               devices=None, slice_budget=None) -> np.ndarray:
+    """numpy in -> numpy out through the C ABI's host path.  ``slice_budget``
+    bounds the device bytes one band holds (source rows with halos + output
+    rows; the reference's banding, aware.py:455-463) -- the result does not
+    depend on it."""
     bits = _bits_of(img.dtype)
     if img.ndim == 2:
         h, w = img.shape
@@ -128,8 +132,9 @@ def _run_numpy(img: np.ndarray, kw: int, kh: int, variant: str, device: int,
                                         len(devices))
     else:
         dev = int(devices[0]) if devices else device
-        rc = lib.tm_median2d_host(src.ctypes.data, src.strides[0], out.ctypes.data,
-                                  out.strides[0], w, h, ch, bits, kw, kh, code, dev)
+        rc = lib.tm_median2d_host_budget(src.ctypes.data, src.strides[0], out.ctypes.data,
+                                         out.strides[0], w, h, ch, bits, kw, kh, code, dev,
+                                         int(slice_budget or 0))
     _lib.check(rc)
     return out
 
@@ -215,7 +220,7 @@ def filter_image(image, k, variant="auto", *, root=None, workers=1, slice_budget
         if 0 in shape:
             raise ValueError(f"image dims must be positive, got {shape[1]}x{shape[0]}")
     out = (_run_torch(img, kern.k_w, kern.k_h, launch, devices) if torch_in
-           else _run_numpy(img, kern.k_w, kern.k_h, launch, device, devices))
+           else _run_numpy(img, kern.k_w, kern.k_h, launch, device, devices, slice_budget))
     if variant == "aware" and (counter is not None or checksums is not None):
         H, W = shape
         itemsize = img.element_size() if torch_in else img.itemsize
@@ -266,7 +271,73 @@ def filter_planes(image, k, variant="auto", **kwargs):
     devices = kwargs.get("devices")
     return (_run_torch(img, kern.k_w, kern.k_h, variant, devices) if torch_in
             else _run_numpy(img, kern.k_w, kern.k_h, variant, int(kwargs.get("device", 0)),
-                            devices))
+                            devices, kwargs.get("slice_budget")))
+
+
+def filter_frames(frames, k, variant="auto", *, devices=None, **kwargs):
+    """Filter a batch of independent frames, (N, H, W) or (N, H, W, C).
+
+    Every frame is filtered exactly like ``filter_planes(frame, k, variant)``
+    (engine.py:55-64); frames are split across ``devices`` (GPU ordinals)
+    with no communication ("batches of frames are split across GPUs").
+    numpy in -> numpy out (one pipelined host call per frame on its device);
+    torch CUDA tensors in -> a tensor on the input's device.
+    """
+    torch_in = _is_torch(frames)
+    arr = frames if torch_in else np.asarray(frames)
+    if arr.ndim not in (3, 4):
+        raise ValueError(f"expected (N, H, W) or (N, H, W, C) frames, got shape {tuple(arr.shape)}")
+    if variant not in VARIANTS:
+        raise ValueError(f"unknown variant {variant!r} (expected one of {VARIANTS})")
+    v = pick_variant(k) if variant == "auto" else variant
+    _validate_like_plane(None, k, v, kwargs.get("root"))
+    kern = as_kernel(k)
+    n_fr, h, w = (int(s) for s in arr.shape[:3])
+    ch = int(arr.shape[3]) if arr.ndim == 4 else 1
+    if ch == 0:
+        raise ValueError("need at least one array to stack")
+    if n_fr == 0:
+        return arr.clone() if torch_in else np.empty_like(arr)
+    if h == 0 or w == 0:
+        raise ValueError(f"image dims must be positive, got {w}x{h}")
+    devs = [int(d) for d in devices] if devices else [int(kwargs.get("device", 0))]
+    if torch_in and arr.is_cuda:
+        import torch
+        src = arr.contiguous()
+        if len(devs) > 1:
+            outs = [_run_torch(src[i].to(f"cuda:{devs[i % len(devs)]}"), kern.k_w, kern.k_h,
+                               variant) for i in range(n_fr)]
+            return torch.stack([o.to(src.device) for o in outs])
+        out = torch.empty_like(src)
+        bits = {torch.uint8: 8, torch.uint16: 16, torch.uint32: 32}.get(src.dtype)
+        if bits is None:
+            raise TypeError(f"unsupported element type {src.dtype}: expected uint8/16/32")
+        esz = src.element_size()
+        lib = _lib.load()
+        with torch.cuda.device(src.device):
+            stream = torch.cuda.current_stream(src.device).cuda_stream
+            for i in range(n_fr):
+                _lib.check(lib.tm_median2d_band(
+                    src[i].data_ptr(), src.stride(1) * esz, h, 0, h, out[i].data_ptr(),
+                    out.stride(1) * esz, w, ch, bits, kern.k_w, kern.k_h,
+                    _lib.VARIANT_CODES[variant], stream))
+        return out
+    if torch_in:
+        import torch
+        return torch.from_numpy(filter_frames(arr.numpy(), k, variant, devices=devices, **kwargs))
+    bits = _bits_of(arr.dtype)
+    src = arr
+    if not (src.strides[-1] == src.itemsize and (ch == 1 or src.strides[2] == ch * src.itemsize)
+            and src.strides[1] > 0 and src.strides[0] >= h * src.strides[1]):
+        src = np.ascontiguousarray(src)
+    out = pinned_empty(arr.shape, arr.dtype)
+    import ctypes
+    ids = (ctypes.c_int32 * len(devs))(*devs)
+    _lib.check(_lib.load().tm_median2d_host_frames(
+        src.ctypes.data, src.strides[1], src.strides[0], out.ctypes.data, out.strides[1],
+        out.strides[0], n_fr, w, h, ch, bits, kern.k_w, kern.k_h, _lib.VARIANT_CODES[variant],
+        ids, len(devs)))
+    return out
 
 
 def _validate_like_plane(probe, k, variant, root) -> None:

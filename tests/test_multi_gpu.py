@@ -141,3 +141,56 @@ def test_ranks_gloo_exchange_cuda_filter(world, k, bits):
     for _, y0, y1, band in parts:
         out[y0:y1] = band
     assert np.array_equal(out, oracle_median_filter_c(img, k).astype(np.int64))
+
+
+@pytest.mark.parametrize("bits,k,shape,n_dev", [(8, 17, (5, 90, 70, 3), 2), (16, 27, (3, 64, 80), 1),
+                                                (32, 9, (4, 33, 47), 3)])
+def test_filter_frames_numpy(bits, k, shape, n_dev):
+    from paper_2507_19926_b200 import filter_frames
+    dt = {8: np.uint8, 16: np.uint16, 32: np.uint32}[bits]
+    rng = np.random.default_rng(k)
+    frames = rng.integers(0, np.iinfo(dt).max, size=shape, dtype=dt, endpoint=True)
+    out = filter_frames(frames, k, devices=_devices(n_dev))
+    assert out.shape == frames.shape and out.dtype == frames.dtype
+    for f in range(shape[0]):
+        assert np.array_equal(out[f], filter_planes(frames[f], k)), f
+        plane = frames[f] if frames.ndim == 3 else np.ascontiguousarray(frames[f][..., 0])
+        got = out[f] if frames.ndim == 3 else out[f][..., 0]
+        assert np.array_equal(got, oracle_median_filter_c(plane, k)), f
+
+
+def test_filter_frames_torch():
+    import torch
+    from paper_2507_19926_b200 import filter_frames
+    rng = np.random.default_rng(1)
+    frames = rng.integers(0, 256, size=(4, 70, 61, 3), dtype=np.uint8)
+    t = torch.from_numpy(frames).cuda()
+    for devs in (None, _devices(2)):
+        out = filter_frames(t, 11, devices=devs)
+        assert out.is_cuda and out.shape == t.shape
+        got = out.cpu().numpy()
+        for f in range(4):
+            for c in range(3):
+                assert np.array_equal(got[f, ..., c],
+                                      oracle_median_filter_c(np.ascontiguousarray(frames[f, ..., c]), 11))
+
+
+def test_filter_frames_validation():
+    from paper_2507_19926_b200 import filter_frames
+    with pytest.raises(ValueError):
+        filter_frames(np.zeros((4, 4), np.uint8), 3)
+    with pytest.raises(ValueError):
+        filter_frames(np.zeros((2, 4, 4), np.uint8), 4)
+    with pytest.raises(ValueError, match="minimum"):
+        filter_frames(np.zeros((2, 4, 4), np.uint8), 7, "aware")
+    assert filter_frames(np.zeros((0, 4, 4), np.uint8), 3).shape == (0, 4, 4)
+
+
+@pytest.mark.parametrize("budget", [1, 4096, 200_000])
+def test_slice_budget_banding(budget):
+    """slice_budget bounds the device bytes per band of the host path; the
+    result never depends on it (test_acceptance.py:126-143)."""
+    img = generate(TestImageSpec("random", 211, 157, 16, seed=4))
+    ref = oracle_median_filter_c(img, 25)
+    assert np.array_equal(filter_image(img, 25, slice_budget=budget), ref)
+    assert np.array_equal(filter_image(img, 25, "aware", slice_budget=budget), ref)

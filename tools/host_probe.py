@@ -45,3 +45,19 @@ x = torch.from_numpy(img).cuda()
 torch.cuda.synchronize()
 print("torch pageable H2D ms", t(lambda: (torch.from_numpy(img).cuda(), torch.cuda.synchronize())))
 print("torch pinned H2D ms", t(lambda: (torch.from_numpy(pin).cuda(non_blocking=True), torch.cuda.synchronize())))
+cudart = torch.cuda.cudart()
+buf = np.random.default_rng(1).integers(0, 256, (H, W, C), dtype=np.uint8)
+def reg():
+    rc = cudart.cudaHostRegister(buf.ctypes.data, buf.nbytes, 0)
+    rc2 = cudart.cudaHostUnregister(buf.ctypes.data)
+print("cudaHostRegister+Unregister 90MB ms", t(reg))
+import threading
+def mt_copy(nt):
+    src = img.reshape(-1); d = dst.reshape(-1); n = src.size
+    def part(i):
+        a, b = n * i // nt, n * (i + 1) // nt
+        np.copyto(d[a:b], src[a:b])
+    th = [threading.Thread(target=part, args=(i,)) for i in range(nt)]
+    [x.start() for x in th]; [x.join() for x in th]
+for nt in (2, 4, 8, 16):
+    print("np copy threads", nt, "ms", t(lambda: mt_copy(nt)))
