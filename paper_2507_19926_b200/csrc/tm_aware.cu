@@ -23,6 +23,7 @@
 // window is the reference's window value for value.
 #include <algorithm>
 #include <cstdio>
+#include <mutex>
 #include <vector>
 
 #include "tm_common.cuh"
@@ -391,13 +392,45 @@ __global__ void finalize_kernel(Job job, const T* __restrict__ cand, int n_cand,
 // ------------------------------------------------------------------------
 // host driver
 
+// The pass buffers come from a private stream-ordered pool per device: freed
+// buffers stay reserved between calls (up to kKeepBytes) without changing the
+// release threshold of the device's default pool, which other users of
+// cudaMallocAsync in the process (e.g. PyTorch) rely on.
+inline cudaMemPool_t pass_pool() {
+  constexpr int kMaxDev = 64;
+  constexpr uint64_t kKeepBytes = 1ull << 30;
+  static std::mutex mu;
+  static cudaMemPool_t pools[kMaxDev] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return nullptr;
+  std::lock_guard<std::mutex> g(mu);
+  if (!pools[dev]) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    if (cudaMemPoolCreate(&pools[dev], &props) != cudaSuccess) {
+      cudaGetLastError();
+      pools[dev] = nullptr;
+      return nullptr;
+    }
+    uint64_t thr = kKeepBytes;
+    cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  return pools[dev];
+}
+
 template <typename T>
 struct Arena {
   cudaStream_t s;
+  cudaMemPool_t pool = pass_pool();
   std::vector<void*> ptrs;
   T* get(long n) {
     void* p = nullptr;
-    if (cudaMallocAsync(&p, (size_t)std::max(n, 1L) * sizeof(T), s) != cudaSuccess) return nullptr;
+    const size_t bytes = (size_t)std::max(n, 1L) * sizeof(T);
+    const cudaError_t e = pool ? cudaMallocFromPoolAsync(&p, bytes, pool, s)
+                               : cudaMallocAsync(&p, bytes, s);
+    if (e != cudaSuccess) return nullptr;
     ptrs.push_back(p);
     return static_cast<T*>(p);
   }
@@ -597,16 +630,6 @@ static int launch_t(const Job& job0, int k, cudaStream_t s, long budget) {
 
 int launch_aware(int bits, const Job& job, int k, cudaStream_t s) {
   const long budget = 3L << 30;  // device bytes per band
-  // keep freed pass buffers in the stream-ordered pool between calls
-  // (the default release threshold of 0 returns them to the OS at every sync)
-  int dev = 0;
-  if (cudaGetDevice(&dev) == cudaSuccess) {
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = ~0ull;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-  }
   switch (bits) {
     case 8: return aware::launch_t<uint8_t>(job, k, s, budget);
     case 16: return aware::launch_t<uint16_t>(job, k, s, budget);

@@ -51,3 +51,34 @@ def render(pattern: str, shape, bits: int, seed: int = 42, device="cuda"):
         noise = torch.randn((h, w), generator=g, device=device) * 200.0 * mx / 65535
         return (base + noise + 0.05 * mx).clamp(0, mx).to(torch.int64).to(tdt)
     raise ValueError(f"unknown pattern {pattern!r} (expected one of {PATTERNS})")
+
+
+def generate_host(pattern: str, width: int, height: int, depth: int = 8, seed: int = 0,
+                  density: float = 0.3):
+    """The reference's test image, bit for bit (reference.py:78-99): numpy,
+    Philox keyed by ``seed`` -- the command line's ``synth:`` inputs."""
+    import numpy as np
+    if pattern not in ("constant", "gradient", "random", "impulse"):
+        raise ValueError(f"unknown pattern {pattern!r} "
+                         "(expected one of ('constant', 'gradient', 'random', 'impulse'))")
+    if depth not in (8, 16, 32):
+        raise ValueError(f"unsupported depth {depth} (expected 8, 16, or 32)")
+    if width < 1 or height < 1:
+        raise ValueError("image dimensions must be positive")
+    if not 0.0 <= density <= 1.0:
+        raise ValueError("density must be within [0, 1]")
+    dtype = {8: np.uint8, 16: np.uint16, 32: np.uint32}[depth]
+    top = np.iinfo(dtype).max
+    if pattern == "constant":
+        return np.full((height, width), 1 << (depth - 1), dtype=dtype)
+    ramp = ((np.arange(height)[:, None] + np.arange(width)[None, :]) & top).astype(dtype)
+    if pattern == "gradient":
+        return ramp
+    rng = np.random.Generator(np.random.Philox(key=seed))
+    if pattern == "random":
+        return rng.integers(0, top, size=(height, width), endpoint=True, dtype=dtype)
+    hit = rng.random(size=ramp.shape) < density
+    salt = rng.random(size=ramp.shape) < 0.5
+    ramp[hit & salt] = top
+    ramp[hit & ~salt] = 0
+    return ramp

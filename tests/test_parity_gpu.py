@@ -213,3 +213,15 @@ def test_host_entry_point_pipelined_bands(bits, k, shape):
         plane = img[..., c] if ch > 1 else img
         got = out[..., c] if ch > 1 else out
         assert np.array_equal(got, oracle_median_filter_c(np.ascontiguousarray(plane), k)), c
+
+
+@pytest.mark.parametrize("bits", [8, 16, 32])
+def test_kernels_above_75(bits):
+    """k = 77..127 (beyond the dispatch table's k <= 75): auto / aware run the
+    reference's multi-pass engine on the GPU, oblivious / oracle the per-pixel
+    selection kernel -- all exact."""
+    img = generate(TestImageSpec("random", 90, 70, bits, seed=77))
+    for k in (77, 101, 127):
+        ref = oracle_median_filter_c(img, k)
+        for variant in ("auto", "aware", "oblivious", "oracle"):
+            assert np.array_equal(filter_image(img, k, variant), ref), (k, variant)
