@@ -11,7 +11,7 @@ import os
 import threading
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libtilemedian_b200.so")
+LIB_PATH = os.environ.get("TMB_LIB", os.path.join(_PKG, "libtilemedian_b200.so"))
 
 VARIANT_CODES = {"auto": 0, "oblivious": 1, "aware": 2, "oracle": 3}
 KERNEL_NAMES = {0: "none", 1: "oblivious", 2: "multipass", 3: "select", 4: "histogram", 5: "rank", 6: "med3"}

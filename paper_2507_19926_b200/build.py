@@ -20,8 +20,10 @@ from . import codegen
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
-BUILD = os.path.join(PKG, "_build")
-LIB = os.path.join(PKG, "libtilemedian_b200.so")
+# experiment builds (e.g. TMB_NVCC_EXTRA=-DTMB_RANK_PROFILE) go elsewhere with
+# TMB_BUILD_DIR / TMB_LIB_OUT; the product library is libtilemedian_b200.so
+BUILD = os.environ.get("TMB_BUILD_DIR", os.path.join(PKG, "_build"))
+LIB = os.environ.get("TMB_LIB_OUT", os.path.join(PKG, "libtilemedian_b200.so"))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",

@@ -48,12 +48,19 @@ namespace {
 
 template <int K, int G>
 struct HistCfg {
-  using S = WarpSweep<K, 256, 2>;  // 3 columns per lane (10-bit fields) measured slower
+  // 3 columns per lane (10-bit fields) while K^2 < 512: a third fewer histogram
+  // updates per output; the packed walk serves all columns at once
+  using S = WarpSweep<K, 256, (K <= 21 ? 3 : 2)>;
   static constexpr int CPL = S::kCPL;
   static constexpr int H = K / 2;
   static constexpr int RING = K + 2 * G + 1;        // next group lands while this one runs
   static constexpr int FW = S::COLS + K - 1;        // footprint columns of the warp
-  static constexpr int RW = ((FW + 3) / 4) * 4 + 8; // ring row bytes (+ slack words)
+  // ring row bytes: the last lane's chunk words end at ((CPL*31)/4 + NC + 1) words
+  // (measured per-byte: every byte of the smem budget counts -- 6 warps/SM need
+  // <= 37888 B per 1-warp CTA)
+  static constexpr int RW0 = ((FW + 3) / 4) * 4;
+  static constexpr int RWL = ((S::kCPL * 31) / 4 + S::NWD) * 4;
+  static constexpr int RW = RW0 > RWL ? RW0 : RWL;
   static constexpr int kRingBytes = RING * RW;
   static constexpr int kWarpBytes = S::kHistBytes + kRingBytes;
   static constexpr int E = (G * FW + 31) / 32;      // prefetch bytes per lane
@@ -160,9 +167,10 @@ constexpr int hist_g() {
 #ifdef TMB_HIST_G
   return TMB_HIST_G;
 #else
-  // ring refill group: measured per k range (k = 19, 21: G 8 -> 4 is +14 %;
-  // k = 25: G 8 -> 2 is +18 %; k <= 17 prefers 8, k >= 33 prefers 4)
-  return K <= 17 ? 8 : (K <= 21 ? 4 : (K <= 31 ? 2 : 4));
+  // ring refill group: measured per k range with 2 columns per lane (k = 19, 21:
+  // G 8 -> 4 is +14 %; k = 25: G 8 -> 2 is +18 %; k >= 33 prefers 4); 4 for the
+  // 3-column lanes (k <= 21) keeps the ring small enough for 6 warps per SM
+  return K <= 21 ? 4 : (K <= 31 ? 2 : 4);
 #endif
 }
 

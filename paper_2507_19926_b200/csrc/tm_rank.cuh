@@ -169,6 +169,9 @@ __global__ void __launch_bounds__(32, 1) rank_kernel(Job job, int R, int n_strip
       const int Y0 = Yi;
       const int sy_base = job.out_y0 + Y0 - C::H;  // source row of footprint row 0
       const int q_end = K + rows - 1;              // footprint rows
+#ifdef TMB_RANK_PROFILE
+      long long _t = clock64();
+#endif
 
       // G footprint rows of samples [q0, q0 + G) into registers.
       auto fetch_raw = [&](int q0, uint32_t (&v)[C::E]) {
@@ -426,9 +429,6 @@ __global__ void __launch_bounds__(32, 1) rank_kernel(Job job, int R, int n_strip
         });
       };
 
-#ifdef TMB_RANK_PROFILE
-      long long _t = clock64();
-#endif
       int sp = 0;  // interval stack depth (warp-uniform); entries (lo, hi, bin width)
       auto push = [&](uint32_t a, uint32_t b, uint32_t w) {
         if (lane == 0) {

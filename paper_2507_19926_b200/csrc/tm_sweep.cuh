@@ -46,11 +46,12 @@ __device__ __forceinline__ void st_hist(uint32_t a, uint32_t v) {
   asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 
-// CPL = output columns per lane sharing one count word: 2 (u16 fields, any K)
-// or 3 (10-bit fields, K^2 <= 1023 i.e. K <= 31; measured slower).
+// CPL = output columns per lane sharing one count word: 2 (16-bit fields) or
+// 3 (10-bit fields).  The walk needs the top bit of every field free, so
+// counts must stay below 2^15 (K <= 181) or 2^9 (K <= 21).
 template <int K, int NB = 256, int CPL = 2>
 struct WarpSweep {
-  static_assert(CPL == 2 || (CPL == 3 && K * K <= 1023), "counts must fit their fields");
+  static_assert(CPL == 2 || (CPL == 3 && K * K < 512), "counts must fit their fields");
   static constexpr int FB = CPL == 2 ? 16 : 10;     // bits per count field
   static constexpr uint32_t FM = (1u << FB) - 1u;
   static constexpr int kCPL = CPL;
@@ -135,70 +136,105 @@ struct WarpSweep {
       red_add(addr_of(co, j), 0u - inc(j));
       red_add(addr_of(ci, j), inc(j));
     }
-    // bl[c] += #entering < m[c] - #leaving < m[c] (before m moves)
+    // bl[c] += #entering < m[c] - #leaving < m[c] (before m moves).  Byte-wise
+    // a < t without a guard bit: d = (a & 0x7F) + 0x80 - (t & 0x7F) per byte
+    // (no borrow across bytes); a < t iff bit 7 of MAJ(~a, t, ~d).  The bytes
+    // of the column's window are summed with dp4a (weights = the window mask),
+    // 128 per key below the threshold.
+    uint32_t a_in[NC], a_out[NC];
+#pragma unroll
+    for (int i = 0; i < NC; i++) {
+      a_in[i] = ci[i] & 0x7F7F7F7Fu;
+      a_out[i] = co[i] & 0x7F7F7F7Fu;
+    }
 #pragma unroll
     for (int c = 0; c < CPL; c++) {
-      const uint32_t mb = (uint32_t)m[c] * 0x01010101u;
-      uint32_t ai = 0, ao = 0;
+      const uint32_t tb = (uint32_t)m[c] * 0x01010101u;
+      const uint32_t cb = 0x80808080u - (tb & 0x7F7F7F7Fu);
+      int acc_i = 0, acc_o = 0;
 #pragma unroll
       for (int i = 0; i < NC; i++) {
         const uint32_t mk = mask(c, i);
         if (mk) {
-          ai += __vsetltu4(ci[i], mb) & mk;
-          ao += __vsetltu4(co[i], mb) & mk;
+          const uint32_t di = a_in[i] + cb, dout = a_out[i] + cb;
+          const uint32_t li = ((~ci[i] & tb) | (~ci[i] & ~di) | (tb & ~di)) & 0x80808080u;
+          const uint32_t lo = ((~co[i] & tb) | (~co[i] & ~dout) | (tb & ~dout)) & 0x80808080u;
+          acc_i = (int)__dp4a(li, mk, (unsigned)acc_i);
+          acc_o = (int)__dp4a(lo, mk, (unsigned)acc_o);
         }
       }
-      bl[c] += (int)__dp4a(ai, 0x01010101u, 0u) - (int)__dp4a(ao, 0x01010101u, 0u);
+      bl[c] += (acc_i - acc_o) >> 7;
     }
     walk();
   }
-  // Move m[c] to the bin holding rank R2, 8 bins per round trip.
-  //   up   (bl < R2):  prefix P_i = h(m) + .. + h(m+i); bins m .. m+i lie
-  //                    wholly below rank R2 iff P_i <= X = R2 - 1 - bl;
-  //                    with n = #{P_i <= X}: median bin m + n, bl += P_{n-1}.
-  //   down (bl >= R2): P_i = h(m-1) + .. + h(m-1-i); bin m-1-i still holds
-  //                    rank R2 or above iff P_i <= X = bl - R2; median bin
-  //                    m - 1 - n, bl -= P_n.
-  // n = 8 means keep going (m += / -= 8, bl +/-= P_7).
+  // Move m[c] to the bin holding rank R2, 8 bins per round trip, all columns
+  // of the lane in one pass of packed-field (SWAR) arithmetic.  Column c scans
+  // the window [s_c, s_c + 8): s_c = m_c going up (bl_c < R2), m_c - 8 going
+  // down.  With B_c = #keys < s_c (bl_c, or bl_c minus the window total) and
+  // P_j the packed prefix sums of the window's counts (P_0 = 0), the median
+  // bin is s_c + n_c - 1 where n_c = #{j in 0..8 : P_j <= T_c},
+  // T_c = R2 - 1 - B_c -- one comparison for all fields at once: with the
+  // top bit of every field free (counts < 2^(FB-1)), (T | guards) - P keeps a
+  // field's guard bit iff P <= T, and no borrow crosses fields.  n_c = 9 or
+  // T_c < 0 mean the median lies beyond the window: the column moves 8 bins
+  // on and the warp runs another round (a converged column's round is
+  // idempotent, so the lanes loop until all agree).
   __device__ __forceinline__ void walk() {
     constexpr int S = 8;
+    constexpr uint32_t ONE = CPL == 2 ? 0x00010001u : 0x00100401u;   // bit 0 of every field
+    constexpr uint32_t GUARD = ONE << (FB - 1);
     for (;;) {
-      bool fin[CPL];
+      int sc[CPL];
+      uint32_t ac[CPL];
 #pragma unroll
       for (int c = 0; c < CPL; c++) {
-        const bool down = bl[c] >= R2;
-        const uint32_t a0 = hb + (uint32_t)(down ? m[c] - 1 : m[c]) * kBinStride;
-        const uint32_t da = down ? (uint32_t)(-(int)kBinStride) : kBinStride;
-        const int X = down ? bl[c] - R2 : R2 - 1 - bl[c];
-        int P[S];
-        int acc = 0;
+        sc[c] = bl[c] >= R2 ? m[c] - S : m[c];
+        ac[c] = hb + (uint32_t)sc[c] * kBinStride;
+      }
+      uint32_t h[S], P[S + 1];
+      P[0] = 0u;
 #pragma unroll
-        for (int i = 0; i < S; i++) {
-          const uint32_t w = ld_hist(a0 + i * da);
-          acc += (int)((w >> (FB * c)) & FM);
-          P[i] = acc;
-        }
-        int n = 0, pin = 0, pout = P[S - 1];  // pin = P_{n-1} (0), pout = P_n (P_7)
+      for (int j = 0; j < S; j++) {
+        uint32_t v = 0u;
 #pragma unroll
-        for (int i = S - 1; i >= 0; i--) {
-          const bool le = P[i] <= X;
-          n += le;
-          pin = (le && pin == 0) ? P[i] : pin;    // largest P_i <= X (P monotone)
-          pout = le ? pout : P[i];                // smallest P_i > X
-        }
-        fin[c] = n < S;
-        if (down) {
-          m[c] -= fin[c] ? n + 1 : S;
-          bl[c] -= pout;
+        for (int c = 0; c < CPL; c++) v |= ld_hist(ac[c] + j * kBinStride) & (FM << (FB * c));
+        h[j] = v;
+        P[j + 1] = P[j] + v;
+      }
+      int B[CPL], T[CPL];
+      uint32_t Tp = GUARD;
+#pragma unroll
+      for (int c = 0; c < CPL; c++) {
+        const int tot = (int)((P[S] >> (FB * c)) & FM);
+        B[c] = bl[c] >= R2 ? bl[c] - tot : bl[c];
+        T[c] = R2 - 1 - B[c];
+        Tp |= (uint32_t)max(T[c], 0) << (FB * c);
+      }
+      uint32_t cnt = ONE, pin = 0u;  // j = 0: P_0 = 0 <= T
+#pragma unroll
+      for (int j = 1; j <= S; j++) {
+        const uint32_t bits = ((Tp - P[j]) >> (FB - 1)) & ONE;
+        cnt += bits;
+        pin += h[j - 1] & (bits * FM);  // sum of h_i with P_{i+1} <= T: P_{n-1}
+      }
+      bool fin = true;
+#pragma unroll
+      for (int c = 0; c < CPL; c++) {
+        const int n = (int)((cnt >> (FB * c)) & FM);
+        if (T[c] < 0) {  // below the window: continue downwards
+          m[c] = sc[c];
+          bl[c] = B[c];
+          fin = false;
+        } else if (n > S) {  // above the window: continue upwards
+          m[c] = sc[c] + S;
+          bl[c] = B[c] + (int)((P[S] >> (FB * c)) & FM);
+          fin = false;
         } else {
-          m[c] += n;
-          bl[c] += pin;
+          m[c] = sc[c] + n - 1;
+          bl[c] = B[c] + (int)((pin >> (FB * c)) & FM);
         }
       }
-      bool all = true;
-#pragma unroll
-      for (int c = 0; c < CPL; c++) all = all && fin[c];
-      if (__all_sync(0xffffffffu, all)) break;
+      if (__all_sync(0xffffffffu, fin)) break;
     }
   }
 };
