@@ -133,13 +133,19 @@ __global__ void __launch_bounds__(32 * WPC) hist8_kernel(Job job, int R, int n_s
     }
     sw.init_median();
     const int x = X0 + C::CPL * tid;
-    auto store = [&](int yrel) {
-      uint8_t* d = dst + (int64_t)(Y0 + yrel) * job.dst_pitch + (int64_t)x * CH;
+    // output pointer advanced one row per store; column predicates fixed per item
+    uint8_t* dp = dst + (int64_t)Y0 * job.dst_pitch + (int64_t)x * CH;
+    const int64_t dpitch = job.dst_pitch;
+    bool col_ok[C::CPL];
+#pragma unroll
+    for (int c = 0; c < C::CPL; c++) col_ok[c] = x + c < W;
+    auto store = [&]() {
 #pragma unroll
       for (int c = 0; c < C::CPL; c++)
-        if (x + c < W) d[c * CH] = (uint8_t)sw.m[c];
+        if (col_ok[c]) dp[c * CH] = (uint8_t)sw.m[c];
+      dp += dpitch;
     };
-    store(0);
+    store();
 
     // ---- sweep down: groups of G output rows --------------------------------
     for (int t0 = 1; t0 < rows; t0 += G) {
@@ -152,7 +158,7 @@ __global__ void __launch_bounds__(32 * WPC) hist8_kernel(Job job, int R, int n_s
         SW::chunks(row(t - 1), tid, co);
         SW::chunks(row(t - 1 + K), tid, ci);
         sw.step(co, ci);
-        store(t);
+        store();
       }
       if (qn < q_end) stash(qn, nxt);
       __syncwarp();
@@ -223,9 +229,13 @@ struct Hist8Table {
   }
 };
 
+#ifdef TMB_HIST_FEW_K  // experiment builds (tools/vbuild.py): a subset of k
+using Hist8All = Hist8Table<15, 17, 21, 25, 33, 49, 75>;
+#else
 using Hist8All = Hist8Table<3, 5, 7, 9, 11, 13, 15, 17, 19, 21, 23, 25, 27, 29, 31, 33, 35, 37,
                             39, 41, 43, 45, 47, 49, 51, 53, 55, 57, 59, 61, 63, 65, 67, 69, 71,
                             73, 75>;
+#endif
 
 }  // namespace
 

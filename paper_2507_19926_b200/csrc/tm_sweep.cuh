@@ -219,20 +219,14 @@ struct WarpSweep {
       }
       bool fin = true;
 #pragma unroll
-      for (int c = 0; c < CPL; c++) {
+      for (int c = 0; c < CPL; c++) {  // branch-free: selects, no reconvergence
         const int n = (int)((cnt >> (FB * c)) & FM);
-        if (T[c] < 0) {  // below the window: continue downwards
-          m[c] = sc[c];
-          bl[c] = B[c];
-          fin = false;
-        } else if (n > S) {  // above the window: continue upwards
-          m[c] = sc[c] + S;
-          bl[c] = B[c] + (int)((P[S] >> (FB * c)) & FM);
-          fin = false;
-        } else {
-          m[c] = sc[c] + n - 1;
-          bl[c] = B[c] + (int)((pin >> (FB * c)) & FM);
-        }
+        const bool below = T[c] < 0;    // below the window: continue downwards from sc
+        const bool above = n > S;       // above the window: continue upwards from sc + S
+        const int add = above ? (int)((P[S] >> (FB * c)) & FM) : (int)((pin >> (FB * c)) & FM);
+        m[c] = below ? sc[c] : sc[c] + (above ? S : n - 1);
+        bl[c] = B[c] + (below ? 0 : add);
+        fin = fin && !below && !above;
       }
       if (__all_sync(0xffffffffu, fin)) break;
     }
