@@ -3,9 +3,12 @@
     python tools/sweep.py --size 4096 --bits 8 16 32 --k 3 5 7 9 11 --variants auto
 
 Times the C ABI on torch CUDA buffers with CUDA events (warm-up, then the
-median of --reps launches), prints one JSON object per point including the
-ALU-roofline fraction against W(k) (the reference op model) and the measured
-min/max issue peak (profiles/r01_minmax_microbench.txt).
+median of --reps launches, L2 flushed with a 256 MiB write before each timed
+launch), samples SM clocks and throttle reasons during every point (bench.py's
+ClockSampler), and prints one JSON object per point including the ALU-roofline
+fraction against W(k) (the reference op model) and the measured min/max issue
+peak (profiles/r01_minmax_microbench.txt), and the HBM roofline against
+MEASURED_PEAKS.json.
 """
 import argparse
 import json
@@ -18,6 +21,7 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2507_19926_b200 import _lib  # noqa: E402
 from paper_2507_19926_b200.program import op_model  # noqa: E402
+from bench import ClockSampler, _peaks  # noqa: E402
 
 MINMAX_PEAK = 18.6e12  # thread-level VIMNMX/s, measured (148 SM x 64/clk x 1.965 GHz)
 TDT = {8: torch.uint8, 16: torch.uint16, 32: torch.uint32}
@@ -37,6 +41,8 @@ def main():
     lib = _lib.load()
     n = a.size
     g = torch.Generator(device="cuda").manual_seed(42)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    hbm_gbs = float(_peaks().get("hbm_gbs", 6650.0))
     for bits in a.bits:
         src = torch.randint(0, 1 << min(bits, 31), (n, n), generator=g, device="cuda",
                             dtype=torch.int64).to(TDT[bits])
@@ -60,23 +66,29 @@ def main():
                     run()
                 torch.cuda.synchronize()
                 times = []
-                for _ in range(a.reps):
-                    e0 = torch.cuda.Event(enable_timing=True)
-                    e1 = torch.cuda.Event(enable_timing=True)
-                    e0.record()
-                    run()
-                    e1.record()
-                    e1.synchronize()
-                    times.append(e0.elapsed_time(e1))
+                with ClockSampler(torch.cuda.current_device()) as clk:
+                    for _ in range(a.reps):
+                        flush.fill_(1)  # evict the image from L2 (untimed)
+                        e0 = torch.cuda.Event(enable_timing=True)
+                        e1 = torch.cuda.Event(enable_timing=True)
+                        e0.record()
+                        run()
+                        e1.record()
+                        e1.synchronize()
+                        times.append(e0.elapsed_time(e1))
                 ms = float(np.median(times))
                 gpx = n * n / ms / 1e6
                 lanes = 2 if bits < 32 else 1
                 roof_alu = MINMAX_PEAK * lanes / W / 1e9
-                roof_hbm = 6540.8e9 / (2 * esz) / 1e9
+                roof_hbm = hbm_gbs / (2 * esz)
+                cs = clk.summary()
                 print(json.dumps({"bits": bits, "k": k, "variant": v, "kernel": kern,
                                   "ms": round(ms, 4), "gpx_s": round(gpx, 2),
                                   "roof_gpx": round(min(roof_alu, roof_hbm), 1),
-                                  "frac": round(gpx / min(roof_alu, roof_hbm), 3)}), flush=True)
+                                  "frac": round(gpx / min(roof_alu, roof_hbm), 3),
+                                  "hbm_frac": round(gpx / roof_hbm, 3),
+                                  "sm_mhz": cs.get("sm_mhz"), "clk_reasons": cs.get("reasons"),
+                                  "l2": "flushed"}), flush=True)
 
 
 if __name__ == "__main__":

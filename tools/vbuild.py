@@ -6,8 +6,8 @@ variant library, reusing the product build's objects for everything else.
 -> paper_2507_19926_b200/libtilemedian_b200_NAME.so (load it with
 TMB_LIB=<path>; tools/sweep.py and bench.py go through _lib.load()).
 """
+import concurrent.futures as cf
 import os
-import shutil
 import subprocess
 import sys
 
@@ -23,19 +23,21 @@ def main():
     os.makedirs(vdir, exist_ok=True)
     objs = []
     targets = {os.path.abspath(os.path.join(B.PKG, s)) for s in srcs}
+    jobs = []
     for src in B._sources():
         obj = B._obj(src)
         if os.path.abspath(src) in targets:
             vobj = os.path.join(vdir, os.path.basename(obj))
-            cmd = [B.NVCC, *B.ARCH, *B.FLAGS, *extra, "-c", src, "-o", vobj]
-            p = subprocess.run(cmd, capture_output=True, text=True)
+            jobs.append([B.NVCC, *B.ARCH, *B.FLAGS, *extra, "-c", src, "-o", vobj])
+            objs.append(vobj)
+        else:
+            objs.append(obj)
+    with cf.ThreadPoolExecutor(max(1, len(jobs))) as pool:  # one nvcc per source
+        for p in pool.map(lambda c: subprocess.run(c, capture_output=True, text=True), jobs):
             if p.returncode:
                 raise SystemExit(p.stderr[-4000:])
             with open(os.path.join(vdir, "ptxas.log"), "a") as f:
                 f.write(p.stderr)
-            objs.append(vobj)
-        else:
-            objs.append(obj)
     lib = os.path.join(B.PKG, f"libtilemedian_b200_{name}.so")
     p = subprocess.run([B.NVCC, *B.ARCH, "-shared", "-o", lib, *objs, "-lcudart"],
                        capture_output=True, text=True)
