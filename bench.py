@@ -239,6 +239,45 @@ def cpu_baseline(cfg, k, seconds=10.0, threads=None, src=None, ours=None):
     return res
 
 
+def reference_python(cfg, k, budget_s=30.0, threads=None):
+    """The UNMODIFIED reference package (baseline/_ref/tilemedian, installed by
+    pip from /root/reference) on a crop of the workload, on this host's cores:
+    its shipped path ``filter_planes(img, k, "auto", workers=n)`` and its
+    fastest engine for this k ("aware" for k >= 9, the brute-force oracle below).
+    None when baseline/_ref is absent.  Reported beside the C port."""
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "tilemedian")):
+        return None
+    if ref_dir not in sys.path:
+        sys.path.insert(0, ref_dir)
+    import tilemedian  # the reference itself
+    H, W, C, bits, _, _ = cfg
+    dt = {8: np.uint8, 16: np.uint16, 32: np.uint32}[bits]
+    threads = threads or len(os.sched_getaffinity(0))
+    rng = np.random.default_rng(3)
+    out = {"cores": threads, "cpu_model": cpu_model(), "unit": "Gpixel/s",
+           "source": "baseline/_ref/tilemedian (pip install of /root/reference, unmodified)"}
+    best = "aware" if k >= 9 else "oracle"
+    t_end = time.perf_counter() + budget_s
+    for name, variant in (("shipped_auto", "auto"), ("best_engine", best)):
+        side, rec = 32, None
+        while time.perf_counter() < t_end:
+            h, w = min(H, side), min(W, side)
+            img = rng.integers(0, np.iinfo(dt).max, size=(h, w, C) if C > 1 else (h, w),
+                               dtype=dt, endpoint=True)
+            kw = {"workers": threads} if variant != "oracle" else {}
+            t0 = time.perf_counter()
+            tilemedian.filter_planes(img, k, variant, **kw)
+            dt_s = time.perf_counter() - t0
+            rec = {"value": h * w * C / dt_s / 1e9, "variant": variant,
+                   "sample": f"{h}x{w}x{C} random crop, one call, {dt_s:.2f} s"}
+            if dt_s > budget_s / 8 or (h == H and w == W):
+                break
+            side *= 2
+        out[name] = rec
+    return out
+
+
 def run_reference(args, cfg, k, rank, world):
     """--impl reference: the reference algorithm's CPU path (oracle port), rank 0 only."""
     if rank != 0:
@@ -268,6 +307,12 @@ def run_reference(args, cfg, k, rank, world):
                          "cpu_model": cpu_model(), "sample": times[-1]["sample"]},
         "e2e": {"value": v, "unit": "Gpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    try:  # the reference package itself, when baseline/_ref travelled with the repo
+        rp = reference_python(cfg, k, threads=threads)
+    except Exception as exc:  # reported, never fatal for the arm
+        rp = {"error": f"{type(exc).__name__}: {exc}"}
+    if rp is not None:
+        line["reference_python"] = rp
     print(json.dumps(line), flush=True)
 
 

@@ -57,6 +57,19 @@ def test_dispatch_table_crossovers():
     assert name(32, 5, 3) == "select"                                  # variant "oracle"
 
 
+def test_oblivious_variant_above_27_is_reported_as_select():
+    """variant "oblivious" runs a comparator-network kernel for k <= 27; above,
+    the exact per-pixel radix selection (the same results) -- and says so."""
+    lib = _lib.load()
+    name = lambda b, k: lib.tm_kernel_name(lib.tm_dispatch_query(b, k, k, 1)).decode()
+    from paper_2507_19926_b200 import dispatch_query
+    import numpy as np
+    for bits, dt in ((8, np.uint8), (16, np.uint16), (32, np.uint32)):
+        assert name(bits, 27) == "oblivious"
+        assert [name(bits, k) for k in (29, 49, 75)] == ["select"] * 3
+        assert dispatch_query(dt, 29, "oblivious") == "select"
+
+
 def test_host_validation_without_gpu():
     """Argument errors are reported before any CUDA call (no GPU needed)."""
     lib = _lib.load()
