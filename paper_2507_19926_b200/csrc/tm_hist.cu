@@ -82,13 +82,39 @@ __global__ void __launch_bounds__(32 * WPC) hist8_kernel(Job job, int R, int n_s
   const int W = job.width, SH = job.src_h, CH = job.channels;
   const int n_items = n_strips * CH * n_segs;
 
-  for (int item = blockIdx.x * WPC + warp; item < n_items; item += gridDim.x * WPC) {
-    const int chan = item % CH;
-    const int strip = (item / CH) % n_strips;
-    const int seg = item / (CH * n_strips);
+  // Work assignment.  n_segs > 0: items of R rows (segment s of a column
+  // strip), grid-stride.  n_segs == 0: the (channel, strip) columns' output
+  // rows laid end to end and cut into one equal piece per warp -- every warp
+  // does the same row count (a piece crossing a strip boundary runs as two
+  // sub-items), so no SM idles at the end.
+  const int gw = blockIdx.x * WPC + warp;
+  int item = gw;
+  const int64_t total = (int64_t)n_strips * CH * job.out_h;
+  int64_t p0 = 0, p1 = 0;
+  if (n_segs == 0) {
+    const int P = gridDim.x * WPC;
+    p0 = total * gw / P;
+    p1 = total * (gw + 1) / P;
+  }
+  for (;;) {
+    int chan, strip, Y0, rows;
+    if (n_segs == 0) {
+      if (p0 >= p1) break;
+      const int64_t ci = p0 / job.out_h;
+      Y0 = (int)(p0 - ci * job.out_h);
+      rows = (int)min((int64_t)(job.out_h - Y0), p1 - p0);
+      chan = (int)(ci % CH);
+      strip = (int)(ci / CH);
+      p0 += rows;
+    } else {
+      if (item >= n_items) break;
+      chan = item % CH;
+      strip = (item / CH) % n_strips;
+      Y0 = (item / (CH * n_strips)) * R;
+      rows = min(R, job.out_h - Y0);
+      item += gridDim.x * WPC;
+    }
     const int X0 = strip * SW::COLS;
-    const int Y0 = seg * R;
-    const int rows = min(R, job.out_h - Y0);
     const uint8_t* src = static_cast<const uint8_t*>(job.src) + chan;
     uint8_t* dst = static_cast<uint8_t*>(job.dst) + chan;
     const int sy_base = job.out_y0 + Y0 - C::H;  // source row of ring row q = 0
@@ -212,10 +238,20 @@ int launch_hist8_k(const Job& job, cudaStream_t stream) {
     }
   }
   const int R = best_R;
-  const int n_segs = (job.out_h + R - 1) / R;
+  int n_segs = (job.out_h + R - 1) / R;
   const long items = (long)n_segs * n_strips * job.channels;
   const long ctas = (items + WPC - 1) / WPC;
-  const int grid = (int)(ctas < slots / WPC ? ctas : slots / WPC);
+  int grid = (int)(ctas < slots / WPC ? ctas : slots / WPC);
+#ifndef TMB_HIST_SEGMENTS
+  // long pieces: one equal piece per resident warp (continuous mode) beats the
+  // best segment count whenever a piece is much longer than the k-row build
+  // it may pay twice (C2: 840 segments on 888 warps -> 888 pieces, +3..5 %)
+  const int64_t total = (int64_t)n_strips * job.channels * job.out_h;
+  if (total / slots >= 4 * (K + 8) && (long)(total / slots) + 2 * (K + 8) < best_cost) {
+    n_segs = 0;
+    grid = (int)(slots / WPC);
+  }
+#endif
   fn<<<grid, 32 * WPC, kSmem, stream>>>(job, R, n_strips, n_segs);
   return (int)cudaGetLastError();
 }

@@ -59,7 +59,11 @@ struct WarpSweep {
   static constexpr int NS = K + CPL - 1;           // keys per lane per row
   static constexpr int NC = (NS + 3) / 4;          // 4-key chunks
   static constexpr int NWD = NC + 1;               // aligned words covering the chunks
-  static constexpr int kPad = 8;                   // zero bins below 0 / above NB - 1
+#ifndef TMB_WALK_S
+#define TMB_WALK_S 8  // bins per walk round trip (measured: 8)
+#endif
+  static constexpr int kWalk = TMB_WALK_S;
+  static constexpr int kPad = kWalk > 8 ? kWalk : 8;  // zero bins below 0 / above NB - 1
   static constexpr int kWords = NB + 2 * kPad;
   static constexpr int kHistBytes = kWords * 32 * 4;
   static constexpr int R2 = (K * K + 1) / 2;       // median rank, 1-based
@@ -180,7 +184,7 @@ struct WarpSweep {
   // on and the warp runs another round (a converged column's round is
   // idempotent, so the lanes loop until all agree).
   __device__ __forceinline__ void walk() {
-    constexpr int S = 8;
+    constexpr int S = kWalk;
     constexpr uint32_t ONE = CPL == 2 ? 0x00010001u : 0x00100401u;   // bit 0 of every field
     constexpr uint32_t GUARD = ONE << (FB - 1);
     for (;;) {

@@ -1,0 +1,12 @@
+# hist8: continuous equal pieces per warp (product) vs best segment count (seg)
+timeout 900 python -m pytest tests -m gpu -x -q -k "hist or planes or c2 or c5 or golden or random_vs_oracle or edge or strided or tall" 2>&1 | tail -2
+for v in "" seg "" seg; do
+  if [ -n "$v" ]; then export TMB_LIB=paper_2507_19926_b200/libtilemedian_b200_$v.so; else unset TMB_LIB; fi
+  timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/b_c2_$v.json 2>&1; python -c "
+import json; d=json.loads(open('gpurun_out/b_c2_$v.json').read().strip().splitlines()[-1]); print('$v C2', round(d['value'],2), 'ms', round(d['ms_per_step'],3), 'clk', d['clocks']['sm_mhz'])"
+  timeout 300 python tools/sweep.py --size 4096 --bits 8 --k 15 17 21 25 33 49 75 --kernels histogram --reps 10 2>&1 | python -c "
+import sys,json
+print('$v', [ (d['k'], d['gpx_s']) for d in map(json.loads, sys.stdin)])"
+  timeout 300 python bench.py --config c5 --k 33 --steps 5 --warmup 3 --no-cpu-baseline 2>&1 | tail -1 | python -c "
+import sys,json; d=json.loads(sys.stdin.read()); print('$v C5k33', round(d['value'],2))"
+done
