@@ -120,24 +120,36 @@ __global__ void __launch_bounds__(32 * WPC) hist8_kernel(Job job, int R, int n_s
     const int sy_base = job.out_y0 + Y0 - C::H;  // source row of ring row q = 0
     const int q_end = K + rows - 1;              // ring rows of this item: [0, q_end)
 
+    // Slot e of a lane fetches group row g_e, footprint column c_e; both and
+    // the clamped column offset are fixed per item (computed once here), so a
+    // fetch costs a row clamp, one wide multiply-add and the load.
+    int g_of[C::E], xo[C::E], ro[C::E];
+#pragma unroll
+    for (int e = 0; e < C::E; e++) {
+      const int idx = tid + e * 32;
+      const int g = idx / C::FW, c = idx - g * C::FW;
+      g_of[e] = idx < G * C::FW ? g : 0x3fffffff;  // an unused slot never passes q < q_end
+      xo[e] = clampi(X0 - C::H + c, 0, W - 1) * CH;
+      ro[e] = g * C::RW + c;                       // byte of the slot in its ring row
+    }
     auto fetch = [&](int q0, uint8_t (&v)[C::E]) {
 #pragma unroll
       for (int e = 0; e < C::E; e++) {
-        const int idx = tid + e * 32;
-        const int g = idx / C::FW, c = idx - (idx / C::FW) * C::FW;
-        if (idx < G * C::FW && q0 + g < q_end) {
-          const int sy = clampi(sy_base + q0 + g, 0, SH - 1);
-          const int sx = clampi(X0 - C::H + c, 0, W - 1);
-          v[e] = __ldg(src + (int64_t)sy * job.src_pitch + (int64_t)sx * CH);
+        if (q0 + g_of[e] < q_end) {
+          const int sy = clampi(sy_base + q0 + g_of[e], 0, SH - 1);
+          v[e] = __ldg(src + (int64_t)sy * job.src_pitch + xo[e]);
         }
       }
     };
     auto stash = [&](int q0, const uint8_t (&v)[C::E]) {
+      // ring rows q0 .. q0 + G - 1 are consecutive modulo RING: one base
+      uint8_t* rb = ring + (q0 % C::RING) * C::RW;
 #pragma unroll
       for (int e = 0; e < C::E; e++) {
-        const int idx = tid + e * 32;
-        const int g = idx / C::FW, c = idx - (idx / C::FW) * C::FW;
-        if (idx < G * C::FW && q0 + g < q_end) ring[((q0 + g) % C::RING) * C::RW + c] = v[e];
+        if (q0 + g_of[e] < q_end) {
+          const int r = (q0 % C::RING) + g_of[e];
+          rb[ro[e] - (r >= C::RING ? C::RING * C::RW : 0)] = v[e];
+        }
       }
     };
     auto row = [&](int q) { return ring + (q % C::RING) * C::RW; };

@@ -173,27 +173,30 @@ __global__ void __launch_bounds__(32, 1) rank_kernel(Job job, int R, int n_strip
       long long _t = clock64();
 #endif
 
-      // G footprint rows of samples [q0, q0 + G) into registers.
+      // G footprint rows of samples [q0, q0 + G) into registers.  Slot e of
+      // a lane reads group row g_e at footprint column c_e; both and the
+      // clamped column offset are fixed per item (computed once here).
+      int g_of[C::E], xo[C::E], c_of[C::E];
+#pragma unroll
+      for (int e = 0; e < C::E; e++) {
+        const int idx = lane + e * 32;
+        const int g = idx / C::FW, c = idx - g * C::FW;
+        g_of[e] = idx < C::G * C::FW ? g : 0x3fffffff;  // an unused slot never passes q < q_end
+        xo[e] = clampi(X0 - C::H + c, 0, W - 1) * CH;
+        c_of[e] = c;
+      }
       auto fetch_raw = [&](int q0, uint32_t (&v)[C::E]) {
 #pragma unroll
         for (int e = 0; e < C::E; e++) {
-          const int idx = lane + e * 32;
-          const int g = idx / C::FW, c = idx - (idx / C::FW) * C::FW;
-          v[e] = (idx < C::G * C::FW && q0 + g < q_end)
-                     ? load_s(src, job, clampi(sy_base + q0 + g, 0, SH - 1),
-                              clampi(X0 - C::H + c, 0, W - 1))
-                     : 0u;
+          v[e] = 0u;
+          if (q0 + g_of[e] < q_end) {
+            const int sy = clampi(sy_base + q0 + g_of[e], 0, SH - 1);
+            v[e] = __ldg(src + (int64_t)sy * job.src_pitch + xo[e]);
+          }
         }
       };
-      auto valid = [&](int q0, int e) {
-        const int idx = lane + e * 32;
-        return idx < C::G * C::FW && q0 + idx / C::FW < q_end;
-      };
-      auto pos_of = [&](int q0, int e) {
-        const int idx = lane + e * 32;
-        const int g = idx / C::FW, c = idx - (idx / C::FW) * C::FW;
-        return (uint32_t)(((q0 + g) << 8) | c);
-      };
+      auto valid = [&](int q0, int e) { return q0 + g_of[e] < q_end; };
+      auto pos_of = [&](int q0, int e) { return (uint32_t)(((q0 + g_of[e]) << 8) | c_of[e]); };
 
       // One sweep over the sub-item with keys from `kf`; `emit(t)` after each row.
       uint32_t fmin = 0xFFFFFFFFu, fmax = 0u;  // the footprint's value range (lane-partial)
@@ -201,10 +204,8 @@ __global__ void __launch_bounds__(32, 1) rank_kernel(Job job, int R, int n_strip
         auto stash = [&](int q0, const uint32_t (&v)[C::E]) {
 #pragma unroll
           for (int e = 0; e < C::E; e++) {
-            const int idx = lane + e * 32;
-            const int g = idx / C::FW, c = idx - (idx / C::FW) * C::FW;
             if (valid(q0, e)) {
-              ring[((q0 + g) % C::RING) * C::KW + c] = kf(v[e]);
+              ring[((q0 + g_of[e]) % C::RING) * C::KW + c_of[e]] = kf(v[e]);
               if (track) {  // every footprint sample is stashed exactly once
                 fmin = min(fmin, v[e]);
                 fmax = max(fmax, v[e]);

@@ -1,0 +1,15 @@
+# cheaper footprint fetch (per-item column offsets) in hist8 and rank: tests + numbers
+timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+for i in 1 2; do
+timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline 2>&1 | tail -1 | python -c "
+import sys,json; d=json.loads(sys.stdin.read()); print('C2', round(d['value'],2), d['clocks']['sm_mhz'])"
+done
+timeout 300 python tools/sweep.py --size 4096 --bits 8 --k 15 17 21 25 33 49 75 --kernels histogram --reps 10 2>&1 | python -c "
+import sys,json
+print([ (d['k'], d['gpx_s']) for d in map(json.loads, sys.stdin)])"
+timeout 600 python tools/patterns.py --size 4096 --bits 16 --k 27 49 75 --patterns random gentle --reps 3 2>&1 | python -c "
+import sys,json
+print([(d['k'], d['pattern'][:4], d['gpx_s']) for d in map(json.loads, sys.stdin)])"
+timeout 600 python tools/patterns.py --size 8192 --bits 32 --k 25 49 75 --patterns random --reps 3 2>&1 | python -c "
+import sys,json
+print([(d['k'], d['pattern'][:4], d['gpx_s']) for d in map(json.loads, sys.stdin)])"
