@@ -186,6 +186,11 @@ __global__ void __launch_bounds__(32 * WPC) hist8_kernel(Job job, int R, int n_s
     store();
 
     // ---- sweep down: groups of G output rows --------------------------------
+    // ring rows of the leaving (t - 1) and entering (t - 1 + K) footprint
+    // rows, advanced one row per step with a wrap (no modulo per step)
+    const uint8_t* ring_end = ring + C::RING * C::RW;
+    const uint8_t* po = row(0);
+    const uint8_t* pi = row(K);
     for (int t0 = 1; t0 < rows; t0 += G) {
       uint8_t nxt[C::E];
       const int qn = K + t0 - 1 + G;  // first ring row of the next group
@@ -193,8 +198,12 @@ __global__ void __launch_bounds__(32 * WPC) hist8_kernel(Job job, int R, int n_s
       const int t1 = min(t0 + G, rows);
       for (int t = t0; t < t1; t++) {
         uint32_t co[SW::NC], ci[SW::NC];
-        SW::chunks(row(t - 1), tid, co);
-        SW::chunks(row(t - 1 + K), tid, ci);
+        SW::chunks(po, tid, co);
+        SW::chunks(pi, tid, ci);
+        po += C::RW;
+        pi += C::RW;
+        if (po == ring_end) po = ring;
+        if (pi == ring_end) pi = ring;
         sw.step(co, ci);
         store();
       }

@@ -199,9 +199,18 @@ struct WarpSweep {
       P[0] = 0u;
 #pragma unroll
       for (int j = 0; j < S; j++) {
-        uint32_t v = 0u;
+        // field c from column c's load: a chain of bit selects (one LOP3 per
+        // extra column; the bits above the top field are zero in every word)
+        uint32_t x[CPL];
 #pragma unroll
-        for (int c = 0; c < CPL; c++) v |= ld_hist(ac[c] + j * kBinStride) & (FM << (FB * c));
+        for (int c = 0; c < CPL; c++) x[c] = ld_hist(ac[c] + j * kBinStride);
+        uint32_t v = x[CPL - 1];
+#pragma unroll
+        for (int c = CPL - 2; c >= 0; c--) {
+          constexpr uint32_t kAll = 0xFFFFFFFFu;
+          const uint32_t lowc = kAll >> (32 - FB * (c + 1));  // fields 0..c
+          v = (x[c] & lowc) | (v & ~lowc);
+        }
         h[j] = v;
         P[j + 1] = P[j] + v;
       }
