@@ -40,7 +40,8 @@ int launch(int kernel, int bits, int k_w, int k_h, const tmb::Job& job, cudaStre
   switch (kernel) {
     case TM_KERNEL_OBLIVIOUS: return find_obl(bits, k_w)->fn(job, s);
     case TM_KERNEL_MULTIPASS: return tmb::launch_aware(bits, job, k_w, s);
-    case TM_KERNEL_HISTOGRAM: return tmb::launch_hist8(job, k_w, s);
+    case TM_KERNEL_HISTOGRAM:
+      return k_w == k_h ? tmb::launch_hist8(job, k_w, s) : tmb::launch_hist8_rect(job, k_w, k_h, s);
     case TM_KERNEL_RANK: return tmb::launch_rank(bits, job, k_w, s);
     case TM_KERNEL_MED3: return tmb::launch_med3(bits, job, s);
     default: return tmb::launch_select(bits, job, k_w, k_h, s);
@@ -55,7 +56,8 @@ bool supports(int kernel, int bits, int kw, int kh) {
     case TM_KERNEL_OBLIVIOUS: return square && find_obl(bits, kw) != nullptr;
     case TM_KERNEL_MULTIPASS: return square && kw >= 9;
     case TM_KERNEL_SELECT: return true;
-    case TM_KERNEL_HISTOGRAM: return square && bits == 8 && tmb::hist8_supports(kw);
+    case TM_KERNEL_HISTOGRAM:
+      return bits == 8 && (square ? tmb::hist8_supports(kw) : tmb::hist8_rect_supports(kw, kh));
     case TM_KERNEL_RANK: return square && tmb::rank_supports(bits, kw);
     case TM_KERNEL_MED3: return square && kw == 3;
     default: return false;
@@ -93,7 +95,11 @@ int route(int bits, int kw, int kh, int variant) {
     case TM_VARIANT_AWARE:
       return (square && kw >= 9) ? aware_kernel(bits, kw) : TM_KERNEL_SELECT;
     default:  // auto
-      return square ? auto_kernel(bits, kw) : TM_KERNEL_SELECT;
+      if (square) return auto_kernel(bits, kw);
+      // rectangular: the 8-bit histogram sweep for windows of >= 81 samples,
+      // else (and for 16/32-bit data) the exact per-pixel selection
+      return (bits == 8 && kw * kh >= 81 && tmb::hist8_rect_supports(kw, kh)) ? TM_KERNEL_HISTOGRAM
+                                                                              : TM_KERNEL_SELECT;
   }
 }
 

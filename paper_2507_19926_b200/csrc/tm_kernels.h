@@ -18,6 +18,8 @@ int launch_select(int bits, const Job& job, int kw, int kh, cudaStream_t s);
 int launch_aware(int bits, const Job& job, int k, cudaStream_t s);
 bool hist8_supports(int k);
 int launch_hist8(const Job& job, int k, cudaStream_t s);
+bool hist8_rect_supports(int kw, int kh);
+int launch_hist8_rect(const Job& job, int kw, int kh, cudaStream_t s);
 bool rank_supports(int bits, int k);
 int launch_rank(int bits, const Job& job, int k, cudaStream_t s);
 int launch_med3(int bits, const Job& job, cudaStream_t s);

@@ -85,11 +85,13 @@ struct WarpSweep {
   }
 
   uint32_t hb;  // shared address of bin 0 of this lane
+  int r2;       // median rank (1-based): R2, or (K * kh + 1) / 2 for a K x kh window
   int m[CPL], bl[CPL];
 
   // `hist` = the warp's kHistBytes region.
-  __device__ __forceinline__ void init(uint32_t* hist, int lane) {
+  __device__ __forceinline__ void init(uint32_t* hist, int lane, int rank = R2) {
     hb = smem_u32(hist + kPad * 32 + lane);
+    r2 = rank;
   }
   __device__ __forceinline__ void zero() {
     for (int b = -kPad; b < NB + kPad; b++) st_hist(hb + b * kBinStride, 0u);
@@ -192,7 +194,7 @@ struct WarpSweep {
       uint32_t ac[CPL];
 #pragma unroll
       for (int c = 0; c < CPL; c++) {
-        sc[c] = bl[c] >= R2 ? m[c] - S : m[c];
+        sc[c] = bl[c] >= r2 ? m[c] - S : m[c];
         ac[c] = hb + (uint32_t)sc[c] * kBinStride;
       }
       uint32_t h[S], P[S + 1];
@@ -219,8 +221,8 @@ struct WarpSweep {
 #pragma unroll
       for (int c = 0; c < CPL; c++) {
         const int tot = (int)((P[S] >> (FB * c)) & FM);
-        B[c] = bl[c] >= R2 ? bl[c] - tot : bl[c];
-        T[c] = R2 - 1 - B[c];
+        B[c] = bl[c] >= r2 ? bl[c] - tot : bl[c];
+        T[c] = r2 - 1 - B[c];
         Tp |= (uint32_t)max(T[c], 0) << (FB * c);
       }
       uint32_t cnt = ONE, pin = 0u;  // j = 0: P_0 = 0 <= T

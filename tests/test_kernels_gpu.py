@@ -14,7 +14,7 @@ from oracle import TestImageSpec, generate, oracle_median_filter_c
 
 pytestmark = pytest.mark.gpu
 
-from paper_2507_19926_b200 import _lib  # noqa: E402
+from paper_2507_19926_b200 import KernelSpec, _lib  # noqa: E402
 
 TDT = {8: torch.uint8, 16: torch.uint16, 32: torch.uint32}
 
@@ -175,3 +175,53 @@ def test_med3_interleaved_and_band():
             assert np.array_equal(dst.cpu().numpy().astype(np.uint16), ref[y0:y1]), (y0, y1)
     finally:
         lib.tm_force_kernel(prev)
+
+
+# rectangular k_w x k_h windows on the 8-bit histogram sweep: both CPL
+# layouts (k_w x k_h < 512 with k_w <= 21 -> 3 columns per lane), tall and
+# wide windows, heights beyond 75, a window taller than the image
+RECT_KS = [(3, 27), (27, 3), (5, 17), (17, 5), (21, 23), (21, 25), (15, 31), (31, 15),
+           (75, 3), (3, 75), (25, 121), (75, 127), (9, 127)]
+
+
+def run_rect(img: np.ndarray, kw: int, kh: int) -> np.ndarray:
+    """auto variant through the C ABI (the reference's Python front end only
+    accepts rectangular kernels whose sides cover its root tile)."""
+    lib = _lib.load()
+    assert lib.tm_kernel_name(lib.tm_dispatch_query(8, kw, kh, 0)).decode() == "histogram"
+    dev = torch.from_numpy(img).cuda()
+    out = torch.empty_like(dev)
+    h, w = img.shape
+    _lib.check(lib.tm_median2d_band(dev.data_ptr(), w, h, 0, h, out.data_ptr(), w, w, 1, 8, kw, kh, 0,
+                                    torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+@pytest.mark.parametrize("kw,kh", RECT_KS)
+def test_histogram_u8_rect(kw, kh):
+    for name, img in images(8, 157, 301, seed=kw * 1000 + kh):
+        ref = oracle_median_filter_c(img, KernelSpec(kw, kh))
+        assert np.array_equal(run_rect(img, kw, kh), ref), (name, kw, kh)
+
+
+def test_histogram_u8_rect_window_taller_than_image():
+    img = np.random.default_rng(4).integers(0, 256, (60, 230), dtype=np.uint8)
+    for kw, kh in ((9, 127), (41, 101)):
+        assert np.array_equal(run_rect(img, kw, kh), oracle_median_filter_c(img, KernelSpec(kw, kh)))
+
+
+def test_histogram_u8_rect_drop_in():
+    """filter_image / filter_planes with a KernelSpec (torch and numpy inputs)."""
+    from paper_2507_19926_b200 import dispatch_query, filter_image, filter_planes
+    rng = np.random.default_rng(11)
+    img = rng.integers(0, 256, (230, 410, 3), dtype=np.uint8)
+    for kw, kh in ((9, 31), (21, 23), (31, 15)):
+        assert dispatch_query(np.uint8, KernelSpec(kw, kh), "auto") == "histogram"
+        out = filter_planes(img, KernelSpec(kw, kh))  # numpy drop-in (host path)
+        for c in range(3):
+            plane = np.ascontiguousarray(img[..., c])
+            ref = oracle_median_filter_c(plane, KernelSpec(kw, kh))
+            assert np.array_equal(out[..., c], ref), (kw, kh, c)
+            got = filter_image(torch.from_numpy(plane).cuda(), KernelSpec(kw, kh)).cpu().numpy()
+            assert np.array_equal(got, ref), (kw, kh, c)
