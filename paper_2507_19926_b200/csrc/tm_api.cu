@@ -42,7 +42,9 @@ int launch(int kernel, int bits, int k_w, int k_h, const tmb::Job& job, cudaStre
     case TM_KERNEL_MULTIPASS: return tmb::launch_aware(bits, job, k_w, s);
     case TM_KERNEL_HISTOGRAM:
       return k_w == k_h ? tmb::launch_hist8(job, k_w, s) : tmb::launch_hist8_rect(job, k_w, k_h, s);
-    case TM_KERNEL_RANK: return tmb::launch_rank(bits, job, k_w, s);
+    case TM_KERNEL_RANK:
+      return k_w == k_h ? tmb::launch_rank(bits, job, k_w, s)
+                        : tmb::launch_rank_rect(bits, job, k_w, k_h, s);
     case TM_KERNEL_MED3: return tmb::launch_med3(bits, job, s);
     default: return tmb::launch_select(bits, job, k_w, k_h, s);
   }
@@ -58,7 +60,8 @@ bool supports(int kernel, int bits, int kw, int kh) {
     case TM_KERNEL_SELECT: return true;
     case TM_KERNEL_HISTOGRAM:
       return bits == 8 && (square ? tmb::hist8_supports(kw) : tmb::hist8_rect_supports(kw, kh));
-    case TM_KERNEL_RANK: return square && tmb::rank_supports(bits, kw);
+    case TM_KERNEL_RANK:
+      return square ? tmb::rank_supports(bits, kw) : tmb::rank_rect_supports(bits, kw, kh);
     case TM_KERNEL_MED3: return square && kw == 3;
     default: return false;
   }
@@ -96,10 +99,13 @@ int route(int bits, int kw, int kh, int variant) {
       return (square && kw >= 9) ? aware_kernel(bits, kw) : TM_KERNEL_SELECT;
     default:  // auto
       if (square) return auto_kernel(bits, kw);
-      // rectangular: the 8-bit histogram sweep for windows of >= 81 samples,
-      // else (and for 16/32-bit data) the exact per-pixel selection
-      return (bits == 8 && kw * kh >= 81 && tmb::hist8_rect_supports(kw, kh)) ? TM_KERNEL_HISTOGRAM
-                                                                              : TM_KERNEL_SELECT;
+      // rectangular: the data-aware sweeps (8-bit histogram, 16/32-bit rank)
+      // for windows of >= 81 samples, else the exact per-pixel selection
+      if (kw * kh >= 81) {
+        if (bits == 8 && tmb::hist8_rect_supports(kw, kh)) return TM_KERNEL_HISTOGRAM;
+        if (bits != 8 && tmb::rank_rect_supports(bits, kw, kh)) return TM_KERNEL_RANK;
+      }
+      return TM_KERNEL_SELECT;
   }
 }
 

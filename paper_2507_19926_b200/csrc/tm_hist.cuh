@@ -268,7 +268,9 @@ int launch_hist8_t(const Job& job, int kh, cudaStream_t stream) {
   // best segment count whenever a piece is much longer than the k-row build
   // it may pay twice (C2: 840 segments on 888 warps -> 888 pieces, +3..5 %)
   const int64_t total = (int64_t)n_strips * job.channels * job.out_h;
-  if (total / slots >= 4 * (kh + 8) && (long)(total / slots) + 2 * (kh + 8) < best_cost) {
+  const int64_t piece = total / slots;
+  const int64_t builds = piece / job.out_h + 2;  // sub-items a piece may span
+  if (piece >= 4 * (kh + 8) && piece + builds * (kh + 8) < best_cost) {
     n_segs = 0;
     grid = (int)(slots / WPC);
   }

@@ -22,6 +22,8 @@ bool hist8_rect_supports(int kw, int kh);
 int launch_hist8_rect(const Job& job, int kw, int kh, cudaStream_t s);
 bool rank_supports(int bits, int k);
 int launch_rank(int bits, const Job& job, int k, cudaStream_t s);
+bool rank_rect_supports(int bits, int kw, int kh);
+int launch_rank_rect(int bits, const Job& job, int kw, int kh, cudaStream_t s);
 int launch_med3(int bits, const Job& job, cudaStream_t s);
 
 }  // namespace tmb

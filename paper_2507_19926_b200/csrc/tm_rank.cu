@@ -38,6 +38,41 @@ int launch_rank_u32_1(int k, const Job& job, cudaStream_t s);
 int launch_rank_u32_2(int k, const Job& job, cudaStream_t s);
 int launch_rank_u32_3(int k, const Job& job, cudaStream_t s);
 
+int launch_rank_rect_u16_0(int kw, int kh, const Job& job, cudaStream_t s);
+int launch_rank_rect_u16_1(int kw, int kh, const Job& job, cudaStream_t s);
+int launch_rank_rect_u16_2(int kw, int kh, const Job& job, cudaStream_t s);
+int launch_rank_rect_u16_3(int kw, int kh, const Job& job, cudaStream_t s);
+int launch_rank_rect_u32_0(int kw, int kh, const Job& job, cudaStream_t s);
+int launch_rank_rect_u32_1(int kw, int kh, const Job& job, cudaStream_t s);
+int launch_rank_rect_u32_2(int kw, int kh, const Job& job, cudaStream_t s);
+int launch_rank_rect_u32_3(int kw, int kh, const Job& job, cudaStream_t s);
+
+// rectangular windows: width 3..75 (templated), height 3..127 (run time; the
+// candidate positions keep footprint rows below 256: R + k_h - 1 <= 254)
+bool rank_rect_supports(int bits, int kw, int kh) {
+  return (bits == 16 || bits == 32) && kw >= 3 && kw <= 75 && (kw & 1) && kh >= 3 && kh <= 127 &&
+         (kh & 1);
+}
+
+int launch_rank_rect(int bits, const Job& job, int kw, int kh, cudaStream_t s) {
+  if (!rank_rect_supports(bits, kw, kh)) return (int)cudaErrorInvalidValue;
+  const int part = ((kw - 3) / 2) % 4;
+  if (bits == 16) {
+    switch (part) {
+      case 0: return launch_rank_rect_u16_0(kw, kh, job, s);
+      case 1: return launch_rank_rect_u16_1(kw, kh, job, s);
+      case 2: return launch_rank_rect_u16_2(kw, kh, job, s);
+      default: return launch_rank_rect_u16_3(kw, kh, job, s);
+    }
+  }
+  switch (part) {
+    case 0: return launch_rank_rect_u32_0(kw, kh, job, s);
+    case 1: return launch_rank_rect_u32_1(kw, kh, job, s);
+    case 2: return launch_rank_rect_u32_2(kw, kh, job, s);
+    default: return launch_rank_rect_u32_3(kw, kh, job, s);
+  }
+}
+
 bool rank_supports(int bits, int k) {
   return (bits == 16 || bits == 32) && k >= 3 && k <= 75 && (k & 1);
 }

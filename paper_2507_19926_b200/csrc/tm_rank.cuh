@@ -133,23 +133,30 @@ static __device__ unsigned long long g_rank_prof[8];  // per translation unit; t
 //      (126 finer buckets; intervals pend on a small stack).
 // Every pixel's median lies in exactly one resolved bucket or slice, and each
 // pass stores only the pixels whose median it resolves.
-template <typename T, int K>
-__global__ void __launch_bounds__(32, 1) rank_kernel(Job job, int R, int n_strips, int n_segs) {
+// K = window width; the height is K (square) or the run-time kh_rt (RT,
+// rectangular K x kh windows, tm_rank_rect_*.cu): it sets the ring rows, the
+// build rows, the row test of a candidate and the median rank.
+template <typename T, int K, bool RT>
+__global__ void __launch_bounds__(32, 1)
+    rank_kernel(Job job, int R, int n_strips, int n_segs, int kh_rt) {
   using C = RankCfg<T, K>;
   using SW = typename C::SW;
   constexpr int NB = C::NB;
   constexpr uint32_t kInner = NB - 2;  // inner bins of a key
   constexpr int kStack = C::kStack;
   extern __shared__ __align__(16) uint32_t smem[];
+  const int KH = RT ? kh_rt : K;                    // window height
+  const int RING = RT ? KH + 2 * C::G + 1 : C::RING;
+  const int ring_bytes = RT ? ((RING * C::KW + 15) / 16) * 16 : C::kRingBytes;
   const int lane = threadIdx.x;
   uint8_t* ring = reinterpret_cast<uint8_t*>(smem) + C::kHistBytes;
-  T* cval = reinterpret_cast<T*>(ring + C::kRingBytes);                  // bucketed candidates
+  T* cval = reinterpret_cast<T*>(ring + ring_bytes);                     // bucketed candidates
   uint16_t* cpos = reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(cval) + C::kValBytes);
   int* start = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(cpos) + C::kPosBytes);
   uint32_t* stk = reinterpret_cast<uint32_t*>(start + NB + 1);          // interval stack
   int* cur = reinterpret_cast<int*>(smem);  // placement cursors: idle histogram words
   SW sw;
-  sw.init(smem, lane);
+  sw.init(smem, lane, (K * KH + 1) / 2);
   const int W = job.width, SH = job.src_h, CH = job.channels;
   const int n_items = n_strips * CH * n_segs;
 
@@ -167,8 +174,8 @@ __global__ void __launch_bounds__(32, 1) rank_kernel(Job job, int R, int n_strip
     {
       const int rows = rows_item;
       const int Y0 = Yi;
-      const int sy_base = job.out_y0 + Y0 - C::H;  // source row of footprint row 0
-      const int q_end = K + rows - 1;              // footprint rows
+      const int sy_base = job.out_y0 + Y0 - KH / 2;  // source row of footprint row 0
+      const int q_end = KH + rows - 1;               // footprint rows
 #ifdef TMB_RANK_PROFILE
       long long _t = clock64();
 #endif
@@ -205,7 +212,7 @@ __global__ void __launch_bounds__(32, 1) rank_kernel(Job job, int R, int n_strip
 #pragma unroll
           for (int e = 0; e < C::E; e++) {
             if (valid(q0, e)) {
-              ring[((q0 + g_of[e]) % C::RING) * C::KW + c_of[e]] = kf(v[e]);
+              ring[((q0 + g_of[e]) % RING) * C::KW + c_of[e]] = kf(v[e]);
               if (track) {  // every footprint sample is stashed exactly once
                 fmin = min(fmin, v[e]);
                 fmax = max(fmax, v[e]);
@@ -213,24 +220,24 @@ __global__ void __launch_bounds__(32, 1) rank_kernel(Job job, int R, int n_strip
             }
           }
         };
-        auto row = [&](int q) { return ring + (q % C::RING) * C::KW; };
+        auto row = [&](int q) { return ring + (q % RING) * C::KW; };
         __syncwarp();
         {
           // prologue: rows [0, K + G), loads double-buffered against stores
           uint32_t va[C::E], vb[C::E];
           fetch_raw(0, va);
           int q = 0;
-          for (; q + C::G < K + C::G; q += 2 * C::G) {
+          for (; q + C::G < KH + C::G; q += 2 * C::G) {
             fetch_raw(q + C::G, vb);
             stash(q, va);
-            if (q + 2 * C::G < K + C::G) fetch_raw(q + 2 * C::G, va);
+            if (q + 2 * C::G < KH + C::G) fetch_raw(q + 2 * C::G, va);
             stash(q + C::G, vb);
           }
-          if (q < K + C::G) stash(q, va);
+          if (q < KH + C::G) stash(q, va);
         }
         sw.zero();
         __syncwarp();
-        for (int q = 0; q < K; q++) {
+        for (int q = 0; q < KH; q++) {
           uint32_t ch[SW::NC];
           SW::chunks(row(q), lane, ch);
           sw.add_row(ch);
@@ -239,13 +246,13 @@ __global__ void __launch_bounds__(32, 1) rank_kernel(Job job, int R, int n_strip
         emit(0);
         for (int t0 = 1; t0 < rows; t0 += C::G) {
           uint32_t nxt[C::E];
-          const int qn = K + t0 - 1 + C::G;
+          const int qn = KH + t0 - 1 + C::G;
           if (qn < q_end) fetch_raw(qn, nxt);
           const int t1 = min(t0 + C::G, rows);
           for (int t = t0; t < t1; t++) {
             uint32_t co[SW::NC], ci[SW::NC];
             SW::chunks(row(t - 1), lane, co);
-            SW::chunks(row(t - 1 + K), lane, ci);
+            SW::chunks(row(t - 1 + KH), lane, ci);
             sw.step(co, ci);
             emit(t);
           }
@@ -285,16 +292,21 @@ __global__ void __launch_bounds__(32, 1) rank_kernel(Job job, int R, int n_strip
         if (x + c < W) dst[(int64_t)(Y0 + t) * job.dst_pitch + (int64_t)(x + c) * CH] = (T)v;
       };
       // Bins [blo, bhi] holding the medians of the sub-item's in-image columns.
+      // Only inner bins count: a pixel whose walk ends in bin 0 / NB-1 has its
+      // median outside the swept interval, so another interval resolves it
+      // (counting those bins would grow the next interval back to the
+      // footprint's range, and the work-list could cycle).  blo > bhi: no
+      // median inside.
       auto range_pass = [&](const KeyFn<NB>& kf, int& blo, int& bhi) {
         int b0 = NB - 1, b1 = 0;
         sweep(kf, [&](int) {
-          if (x < W) {
-            b0 = min(b0, sw.m[0]);
-            b1 = max(b1, sw.m[0]);
-          }
-          if (x + 1 < W) {
-            b0 = min(b0, sw.m[1]);
-            b1 = max(b1, sw.m[1]);
+#pragma unroll
+          for (int c = 0; c < 2; c++) {
+            const int b = sw.m[c];
+            if (x + c < W && b >= 1 && b <= NB - 2) {
+              b0 = min(b0, b);
+              b1 = max(b1, b);
+            }
           }
         });
         blo = (int)warp_min((uint32_t)b0);
@@ -399,14 +411,14 @@ __global__ void __launch_bounds__(32, 1) rank_kernel(Job job, int R, int n_strip
             const int b = sw.m[c];
             if (b >= ba && b <= bb) {
               // r'-th in-window candidate of bucket b, in sorted order
-              int need = SW::R2 - sw.bl[c];
+              int need = sw.r2 - sw.bl[c];
               uint32_t v = 0;
               const int cx = 2 * lane + c;  // window columns [cx, cx + K), rows [t, t + K)
               // 4 candidates per round (independent loads), then the exact hit
               const uint32_t pbase = ((uint32_t)t << 8) | (uint32_t)cx;
               auto inwin = [&](uint32_t p) -> int {
                 const uint32_t d = p - pbase;  // column offset in bits 0..7 (row checked apart)
-                return (d & 0xFFu) < (uint32_t)K && ((p >> 8) - (uint32_t)t) < (uint32_t)K;
+                return (d & 0xFFu) < (uint32_t)K && ((p >> 8) - (uint32_t)t) < (uint32_t)KH;
               };
               int i = start[b] - base;
               const int i1 = start[b + 1] - base;
@@ -570,6 +582,7 @@ __global__ void __launch_bounds__(32, 1) rank_kernel(Job job, int R, int n_strip
           const KeyFn<NB> km{lo, hi, (uint32_t)(((uint64_t)kInner << 32) / span2), 1, 0};
           int b0, b1;
           range_pass(km, b0, b1);
+          if (b0 > b1) continue;  // no median inside [lo, hi]
           uint32_t t0 = 0xFFFFFFFFu, t1 = 0u;
           scan([&](uint32_t v, uint32_t) {
             const int kb = km(v);
@@ -607,14 +620,22 @@ __global__ void __launch_bounds__(32, 1) rank_kernel(Job job, int R, int n_strip
   }
 }
 
-template <typename T, int K>
-int launch_rank_k(const Job& job, cudaStream_t stream) {
+// Square K x K (RT = false, kh = K) or rectangular K x kh (RT = true).
+template <typename T, int K, bool RT = false>
+int launch_rank_k(const Job& job, cudaStream_t stream, int kh = K) {
   using C = RankCfg<T, K>;
-  constexpr int kSmem = C::kWarpBytes;
-  static_assert(kSmem <= 227 * 1024, "rank kernel does not fit in shared memory");
-  auto fn = rank_kernel<T, K>;
-  static LaunchCache cache;
-  const LaunchInfo li = cache.get(fn, 32, kSmem);
+  static_assert(C::kWarpBytes <= 227 * 1024, "rank kernel does not fit in shared memory");
+  const int kSmem = RT ? C::kWarpBytes - C::kRingBytes +
+                             (((kh + 2 * C::G + 1) * C::KW + 15) / 16) * 16
+                       : C::kWarpBytes;
+  auto fn = rank_kernel<T, K, RT>;
+  LaunchInfo li;
+  if (!RT) {
+    static LaunchCache cache;
+    li = cache.get(fn, 32, kSmem);
+  } else {  // the ring (and so the occupancy) depends on kh
+    li = launch_info(fn, 32, kSmem);
+  }
   if (li.err != cudaSuccess) return (int)li.err;
   const int sms = li.sms, occ = li.occ;
   const int n_strips = (job.width + 63) / 64;
@@ -628,7 +649,7 @@ int launch_rank_k(const Job& job, cudaStream_t stream) {
     const long items = (long)segs * n_strips * job.channels;
     const long waves = (items + slots - 1) / slots;
     // two sweeps of (rows + ~K build) each
-    const long cost = waves * (long)(R + K + 8);
+    const long cost = waves * (long)(R + kh + 8);
     if (cost < best_cost) {
       best_cost = cost;
       best_R = R;
@@ -638,7 +659,7 @@ int launch_rank_k(const Job& job, cudaStream_t stream) {
   const int n_segs = (job.out_h + R - 1) / R;
   const long items = (long)n_segs * n_strips * job.channels;
   const int grid = (int)(items < slots ? items : slots);
-  fn<<<grid, 32, kSmem, stream>>>(job, R, n_strips, n_segs);
+  fn<<<grid, 32, kSmem, stream>>>(job, R, n_strips, n_segs, kh);
   return (int)cudaGetLastError();
 }
 

@@ -88,6 +88,14 @@ def test_histogram_u8_tall_image_many_segments():
         assert np.array_equal(run_forced("histogram", img, k), oracle_median_filter_c(img, k)), k
 
 
+def test_histogram_u8_wide_short_image_pieces_span_strips():
+    """Wide and short: the launcher's equal pieces per warp are shorter than a
+    strip's rows or span several strips (sub-items with their own builds)."""
+    img = np.random.default_rng(21).integers(0, 256, (100, 60000), dtype=np.uint8)
+    for k in (9, 17):
+        assert np.array_equal(run_forced("histogram", img, k), oracle_median_filter_c(img, k)), k
+
+
 RANK_KS = [3, 9, 17, 29, 33, 47, 75]
 
 
@@ -225,3 +233,36 @@ def test_histogram_u8_rect_drop_in():
             assert np.array_equal(out[..., c], ref), (kw, kh, c)
             got = filter_image(torch.from_numpy(plane).cuda(), KernelSpec(kw, kh)).cpu().numpy()
             assert np.array_equal(got, ref), (kw, kh, c)
+
+
+RANK_RECT_KS = [(5, 17), (17, 5), (9, 33), (33, 9), (27, 49), (49, 27), (75, 3), (3, 75), (25, 127)]
+
+
+def run_rect_any(img: np.ndarray, kw: int, kh: int, expect: str) -> np.ndarray:
+    lib = _lib.load()
+    bits = img.dtype.itemsize * 8
+    assert lib.tm_kernel_name(lib.tm_dispatch_query(bits, kw, kh, 0)).decode() == expect
+    dev = torch.from_numpy(img.astype(np.int64)).to(TDT[bits]).cuda()
+    out = torch.empty_like(dev)
+    h, w = img.shape
+    pitch = w * img.itemsize
+    _lib.check(lib.tm_median2d_band(dev.data_ptr(), pitch, h, 0, h, out.data_ptr(), pitch, w, 1, bits,
+                                    kw, kh, 0, torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    return out.cpu().numpy().astype(img.dtype)
+
+
+@pytest.mark.parametrize("bits", [16, 32])
+@pytest.mark.parametrize("kw,kh", RANK_RECT_KS)
+def test_rank_rect(bits, kw, kh):
+    """16/32-bit rectangular windows on the rank sweeps (run-time height)."""
+    for name, img in images(bits, 157, 301, seed=kw * 1000 + kh):
+        ref = oracle_median_filter_c(img, KernelSpec(kw, kh))
+        assert np.array_equal(run_rect_any(img, kw, kh, "rank"), ref), (bits, name, kw, kh)
+
+
+def test_rect_small_windows_use_select():
+    img = np.random.default_rng(2).integers(0, 1 << 16, (90, 130), dtype=np.uint16)
+    for kw, kh in ((3, 5), (5, 9), (3, 25)):
+        ref = oracle_median_filter_c(img, KernelSpec(kw, kh))
+        assert np.array_equal(run_rect_any(img, kw, kh, "select"), ref), (kw, kh)
