@@ -266,3 +266,17 @@ def test_rect_small_windows_use_select():
     for kw, kh in ((3, 5), (5, 9), (3, 25)):
         ref = oracle_median_filter_c(img, KernelSpec(kw, kh))
         assert np.array_equal(run_rect_any(img, kw, kh, "select"), ref), (kw, kh)
+
+
+def test_data_aware_fuzz_short():
+    """A short randomised run of tools/fuzz_rank.py (value distributions that
+    stress the rank work-list: narrow bands, few values, impulse densities,
+    steps, smooth fields, mixtures; square and rectangular windows)."""
+    import subprocess
+    import sys
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    p = subprocess.run([sys.executable, os.path.join(root, "tools", "fuzz_rank.py"), "--seconds", "20",
+                        "--seed", "7"], capture_output=True, text=True, timeout=300)
+    assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-2000:]
+    assert "0 mismatches" in p.stdout
