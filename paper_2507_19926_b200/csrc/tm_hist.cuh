@@ -22,6 +22,7 @@
 // every resident warp one equal piece of the columns' rows laid end to end;
 // short ones are cut into the segment count with the smallest makespan.
 #pragma once
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 #include <cuda_runtime.h>
@@ -75,29 +76,44 @@ __global__ void __launch_bounds__(32 * WPC)
   const int n_items = n_strips * CH * n_segs;
 
   // Work assignment.  n_segs > 0: items of R rows (segment s of a column
-  // strip), grid-stride.  n_segs == 0: the (channel, strip) columns' output
-  // rows laid end to end and cut into one equal piece per warp -- every warp
-  // does the same row count (a piece crossing a strip boundary runs as two
-  // sub-items), so no SM idles at the end.
+  // strip), grid-stride.  n_segs < 0: continuous mode with blocks of
+  // nsg = -n_segs adjacent strips -- the blocks' output rows laid end to end
+  // and cut into one equal piece per group of nsg x CH consecutive warps, the
+  // group's warps filtering (strip in block, channel) of the same rows side
+  // by side: every warp does the same row count (a piece crossing a block
+  // boundary runs as two sub-items), so no SM idles at the end, and the halo
+  // columns of neighbouring strips and the channels of interleaved rows are
+  // read from L2 by concurrent warps (each line leaves DRAM about once, output
+  // sectors fill in L2 before write-back).
   const int gw = blockIdx.x * WPC + warp;
   int item = gw;
-  const int64_t total = (int64_t)n_strips * CH * job.out_h;
+  int sub_strip = 0, sub_chan = 0, nsg = 1;
   int64_t p0 = 0, p1 = 0;
-  if (n_segs == 0) {
-    const int P = gridDim.x * WPC;
-    p0 = total * gw / P;
-    p1 = total * (gw + 1) / P;
+  if (n_segs < 0) {
+    nsg = -n_segs;
+    const int gsize = nsg * CH;
+    const int groups = gridDim.x * WPC / gsize;  // the last < gsize warps idle
+    const int grp = gw / gsize;
+    const int sub = gw - grp * gsize;
+    sub_chan = sub % CH;
+    sub_strip = sub / CH;
+    if (grp < groups) {
+      const int64_t total = (int64_t)((n_strips + nsg - 1) / nsg) * job.out_h;
+      p0 = total * grp / groups;
+      p1 = total * (grp + 1) / groups;
+    }
   }
   for (;;) {
     int chan, strip, Y0, rows;
-    if (n_segs == 0) {
+    if (n_segs < 0) {
       if (p0 >= p1) break;
-      const int64_t ci = p0 / job.out_h;
-      Y0 = (int)(p0 - ci * job.out_h);
+      const int64_t bi = p0 / job.out_h;
+      Y0 = (int)(p0 - bi * job.out_h);
       rows = (int)min((int64_t)(job.out_h - Y0), p1 - p0);
-      chan = (int)(ci % CH);
-      strip = (int)(ci / CH);
+      chan = sub_chan;
+      strip = (int)bi * nsg + sub_strip;
       p0 += rows;
+      if (strip >= n_strips) continue;  // the last block is partial
     } else {
       if (item >= n_items) break;
       chan = item % CH;
@@ -267,11 +283,15 @@ int launch_hist8_t(const Job& job, int kh, cudaStream_t stream) {
   // long pieces: one equal piece per resident warp (continuous mode) beats the
   // best segment count whenever a piece is much longer than the k-row build
   // it may pay twice (C2: 840 segments on 888 warps -> 888 pieces, +3..5 %)
-  const int64_t total = (int64_t)n_strips * job.channels * job.out_h;
-  const int64_t piece = total / slots;
+  // groups of nsg adjacent strips x CH channels (about 8 warps)
+  const int nsg = std::max(1, std::min(n_strips, 8 / std::max(1, job.channels)));
+  const long gsize = (long)nsg * job.channels;
+  const long groups = slots / gsize;
+  const int64_t blocks = (n_strips + nsg - 1) / nsg;
+  const int64_t piece = groups > 0 ? blocks * job.out_h / groups : 0;
   const int64_t builds = piece / job.out_h + 2;  // sub-items a piece may span
-  if (piece >= 4 * (kh + 8) && piece + builds * (kh + 8) < best_cost) {
-    n_segs = 0;
+  if (groups > 0 && piece >= 4 * (kh + 8) && piece + builds * (kh + 8) < best_cost) {
+    n_segs = -nsg;
     grid = (int)(slots / WPC);
   }
 #endif

@@ -419,8 +419,8 @@ int host_chunk(const HostArgs& a, int device, int ya, int yb) {
     for (int b = 0; b < nb; b++) {
       e = cudaEventSynchronize(r.ev_d2h[b]);
       if (e != cudaSuccess) return set_error(TM_ECUDA, "kernel or copy failed: %s", cudaGetErrorString(e));
-const double tc = g_trace ? now_ms() : 0.0;
-            pool.copy2d(a.dst + (int64_t)y[b] * a.dst_pitch, a.dst_pitch,
+      const double tc = g_trace ? now_ms() : 0.0;
+      pool.copy2d(a.dst + (int64_t)y[b] * a.dst_pitch, a.dst_pitch,
                   pout + (size_t)(y[b] - ya) * row, row, row, y[b + 1] - y[b]);
       if (g_trace) t_copy_out += now_ms() - tc;
     }
