@@ -7,7 +7,7 @@ computed by hand-written CUDA kernels behind a C ABI
 (``include/tilemedian_b200.h``).  See DESIGN.md.
 """
 from .engine import (AUTO_CROSSOVER, VARIANTS, dispatch_query, filter_frames, filter_image,
-                     filter_planes, pick_variant)
+                     filter_planes, pick_variant, pinned_empty)
 from .geometry import KernelSpec, TileDims, retention_window, root_tile_size
 from .model import ComparisonCounter, comparison_count
 from .program import build_program, op_model
@@ -16,6 +16,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "AUTO_CROSSOVER", "VARIANTS", "filter_image", "filter_planes", "filter_frames", "pick_variant",
+    "pinned_empty",
     "dispatch_query", "KernelSpec", "TileDims", "retention_window", "root_tile_size",
     "ComparisonCounter", "comparison_count", "build_program", "op_model", "__version__",
 ]
