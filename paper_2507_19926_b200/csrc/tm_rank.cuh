@@ -81,17 +81,21 @@ __device__ __forceinline__ uint32_t load_s(const T* src, const Job& job, int y, 
 //                           value per bin, hi - lo <= NB - 3);
 //   f > 0  (interval pass): 0 / NB-1 outside [lo, hi], 1 + floor((v - lo) *
 //                           (NB - 2) / span) inside (monotone in v).
-template <int NB>
+// The mode F is a template parameter: every sweep / scan is compiled for the
+// key function it uses (no per-sample mode branches).
+template <int NB, int F>
 struct KeyFn {
   uint32_t lo, hi;
   uint32_t mul;  // f > 0: bin = (v - lo) * mul >> 32, all NB - 2 inner bins in use
-  int f;
   int shift;
   __device__ __forceinline__ uint8_t operator()(uint32_t v) const {
-    if (f < 0) return v < lo ? 0 : (uint8_t)min((v - lo) >> shift, (uint32_t)(NB - 1));
-    if (v < lo) return 0;
-    if (v > hi) return NB - 1;
-    return (uint8_t)(1 + (f == 0 ? v - lo : __umulhi(v - lo, mul)));
+    if constexpr (F < 0) {
+      return v < lo ? 0 : (uint8_t)min((v - lo) >> shift, (uint32_t)(NB - 1));
+    } else {
+      if (v < lo) return 0;
+      if (v > hi) return NB - 1;
+      return (uint8_t)(1 + (F == 0 ? v - lo : __umulhi(v - lo, mul)));
+    }
   }  // f > 0: the smallest value whose key is >= b (1 <= b <= NB - 1); hi + 1
   // (mod 2^32) when no value of [lo, hi] gets there.  Exact: key(v) >= b iff
   // (v - lo) * mul >= (b - 1) * 2^32.
@@ -193,12 +197,19 @@ __global__ void __launch_bounds__(32, 1)
         c_of[e] = c;
       }
       auto fetch_raw = [&](int q0, uint32_t (&v)[C::E]) {
+        if constexpr (C::G == 1) {  // one footprint row: one row pointer per fetch
+          const T* rp = src + (int64_t)clampi(sy_base + q0, 0, SH - 1) * job.src_pitch;
+          const bool row_ok = q0 < q_end;
 #pragma unroll
-        for (int e = 0; e < C::E; e++) {
-          v[e] = 0u;
-          if (q0 + g_of[e] < q_end) {
-            const int sy = clampi(sy_base + q0 + g_of[e], 0, SH - 1);
-            v[e] = __ldg(src + (int64_t)sy * job.src_pitch + xo[e]);
+          for (int e = 0; e < C::E; e++) v[e] = (row_ok && g_of[e] == 0) ? __ldg(rp + xo[e]) : 0u;
+        } else {
+#pragma unroll
+          for (int e = 0; e < C::E; e++) {
+            v[e] = 0u;
+            if (q0 + g_of[e] < q_end) {
+              const int sy = clampi(sy_base + q0 + g_of[e], 0, SH - 1);
+              v[e] = __ldg(src + (int64_t)sy * job.src_pitch + xo[e]);
+            }
           }
         }
       };
@@ -207,7 +218,7 @@ __global__ void __launch_bounds__(32, 1)
 
       // One sweep over the sub-item with keys from `kf`; `emit(t)` after each row.
       uint32_t fmin = 0xFFFFFFFFu, fmax = 0u;  // the footprint's value range (lane-partial)
-      auto sweep = [&](const KeyFn<NB>& kf, auto&& emit, bool track = false) {
+      auto sweep = [&](const auto& kf, auto&& emit, bool track = false) {
         auto stash = [&](int q0, const uint32_t (&v)[C::E]) {
 #pragma unroll
           for (int e = 0; e < C::E; e++) {
@@ -297,7 +308,7 @@ __global__ void __launch_bounds__(32, 1)
       // (counting those bins would grow the next interval back to the
       // footprint's range, and the work-list could cycle).  blo > bhi: no
       // median inside.
-      auto range_pass = [&](const KeyFn<NB>& kf, int& blo, int& bhi) {
+      auto range_pass = [&](const auto& kf, int& blo, int& bhi) {
         int b0 = NB - 1, b1 = 0;
         sweep(kf, [&](int) {
 #pragma unroll
@@ -315,7 +326,7 @@ __global__ void __launch_bounds__(32, 1)
       // Exact slice: one value per bin over [a, b] (b - a < NB - 2); stores
       // every pixel whose median lies in [a, b].
       auto slice = [&](uint32_t a, uint32_t b) {
-        const KeyFn<NB> kx{a, b, 0u, 0, 0};
+        const KeyFn<NB, 0> kx{a, b, 0u, 0};
         sweep(kx, [&](int t) {
 #pragma unroll
           for (int c = 0; c < 2; c++) {
@@ -334,7 +345,7 @@ __global__ void __launch_bounds__(32, 1)
       // sweep; stores every pixel whose median lies in those buckets -- its
       // walk ends in bucket b with residual rank R2 - #keys < b, and the median
       // is that rank among b's in-window candidates in sorted order.
-      auto resolve = [&](const KeyFn<NB>& kf, int ba, int bb) {
+      auto resolve = [&](const auto& kf, int ba, int bb) {
         const int base = start[ba];
         for (int b = ba + lane; b <= bb; b += 32) cur[b] = start[b] - base;
         __syncwarp();
@@ -467,7 +478,7 @@ __global__ void __launch_bounds__(32, 1)
       if (gmax - gmin < kInner) {
         // at most 126 values guessed: one value per bin -- pixels whose median
         // lies inside are final; the clamped ends become intervals
-        const KeyFn<NB> kx{gmin, gmax, 0u, 0, 0};
+        const KeyFn<NB, 0> kx{gmin, gmax, 0u, 0};
         int lo_any = 0, hi_any = 0;
         sweep(kx, [&](int t) {
 #pragma unroll
@@ -487,7 +498,7 @@ __global__ void __launch_bounds__(32, 1)
       } else {
         const int s = 25 - __clz(gmax - gmin);  // bit length - 7 (>= 0: the range is >= 126)
         int blo = NB - 1, bhi = 0;
-        sweep(KeyFn<NB>{gmin, gmax, 0u, -1, s}, [&](int) {
+        sweep(KeyFn<NB, -1>{gmin, gmax, 0u, s}, [&](int) {
           if (x < W) {
             blo = min(blo, sw.m[0]);
             bhi = max(bhi, sw.m[0]);
@@ -524,7 +535,7 @@ __global__ void __launch_bounds__(32, 1)
         // (bucket, lane) at word bucket * 32 + lane, no contention -- plus
         // their exact value range
         const uint32_t mul = (uint32_t)(((uint64_t)kInner << 32) / span);
-        const KeyFn<NB> kf{lo, hi, mul, 1, 0};
+        const KeyFn<NB, 1> kf{lo, hi, mul, 0};
         uint32_t* lc = smem;
         for (int b = 0; b < NB; b++) lc[b * 32 + lane] = 0;
         __syncwarp();
@@ -579,7 +590,7 @@ __global__ void __launch_bounds__(32, 1)
           // the candidates reach far beyond the medians (outliers, gaps):
           // an interval sweep of 126 buckets over [lo, hi], then the samples
           // of the buckets holding medians give the next interval
-          const KeyFn<NB> km{lo, hi, (uint32_t)(((uint64_t)kInner << 32) / span2), 1, 0};
+          const KeyFn<NB, 1> km{lo, hi, (uint32_t)(((uint64_t)kInner << 32) / span2), 0};
           int b0, b1;
           range_pass(km, b0, b1);
           if (b0 > b1) continue;  // no median inside [lo, hi]
