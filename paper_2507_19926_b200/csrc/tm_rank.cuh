@@ -220,10 +220,13 @@ __global__ void __launch_bounds__(32, 1)
       uint32_t fmin = 0xFFFFFFFFu, fmax = 0u;  // the footprint's value range (lane-partial)
       auto sweep = [&](const auto& kf, auto&& emit, bool track = false) {
         auto stash = [&](int q0, const uint32_t (&v)[C::E]) {
+          uint8_t* rb = ring + (q0 % RING) * C::KW;  // G = 1: one ring row
 #pragma unroll
           for (int e = 0; e < C::E; e++) {
             if (valid(q0, e)) {
-              ring[((q0 + g_of[e]) % RING) * C::KW + c_of[e]] = kf(v[e]);
+              uint8_t* dstp = C::G == 1 ? rb + c_of[e]
+                                        : ring + ((q0 + g_of[e]) % RING) * C::KW + c_of[e];
+              *dstp = kf(v[e]);
               if (track) {  // every footprint sample is stashed exactly once
                 fmin = min(fmin, v[e]);
                 fmax = max(fmax, v[e]);
@@ -255,6 +258,11 @@ __global__ void __launch_bounds__(32, 1)
         }
         sw.init_median();
         emit(0);
+        // ring rows of the leaving / entering footprint rows, advanced with a
+        // wrap instead of a modulo per step
+        const uint8_t* ring_end = ring + RING * C::KW;
+        const uint8_t* po = row(0);
+        const uint8_t* pi = row(KH);
         for (int t0 = 1; t0 < rows; t0 += C::G) {
           uint32_t nxt[C::E];
           const int qn = KH + t0 - 1 + C::G;
@@ -262,8 +270,12 @@ __global__ void __launch_bounds__(32, 1)
           const int t1 = min(t0 + C::G, rows);
           for (int t = t0; t < t1; t++) {
             uint32_t co[SW::NC], ci[SW::NC];
-            SW::chunks(row(t - 1), lane, co);
-            SW::chunks(row(t - 1 + KH), lane, ci);
+            SW::chunks(po, lane, co);
+            SW::chunks(pi, lane, ci);
+            po += C::KW;
+            pi += C::KW;
+            if (po == ring_end) po = ring;
+            if (pi == ring_end) pi = ring;
             sw.step(co, ci);
             emit(t);
           }
