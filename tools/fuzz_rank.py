@@ -83,10 +83,10 @@ def run(img, bits, kw, kh, kernel):
     out = torch.empty_like(dev)
     h, w = img.shape
     pitch = w * img.itemsize
-    prev = lib.tm_force_kernel(_lib.KERNEL_CODES[kernel])
+    prev = lib.tm_force_kernel(_lib.KERNEL_CODES[kernel] if kernel else 0)
     try:
         got = lib.tm_kernel_name(lib.tm_dispatch_query(bits, kw, kh, 0)).decode()
-        assert got == kernel, (got, kernel)
+        assert kernel is None or got == kernel, (got, kernel)
         _lib.check(lib.tm_median2d_band(dev.data_ptr(), pitch, h, 0, h, out.data_ptr(), pitch, w, 1,
                                         bits, kw, kh, 0, torch.cuda.current_stream().cuda_stream))
         torch.cuda.synchronize()
@@ -100,6 +100,9 @@ def main():
     ap.add_argument("--seconds", type=float, default=240)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--hang", type=float, default=20)
+    ap.add_argument("--all-kernels", action="store_true",
+                    help="also draw k <= 27 windows for the oblivious / med3 kernels and "
+                         "small windows for select (auto routing, not forced)")
     a = ap.parse_args()
     threading.Thread(target=watchdog, args=(a.hang,), daemon=True).start()
     rng = np.random.default_rng(a.seed)
@@ -109,12 +112,17 @@ def main():
         bits = int(rng.choice([8, 16, 16, 32, 32]))
         kw = int(rng.integers(1, 38)) * 2 + 1
         kh = kw if rng.random() < 0.6 else int(rng.integers(1, 64)) * 2 + 1
-        if kw * kh < 81:
+        kernel = "histogram" if bits == 8 else "rank"
+        if a.all_kernels and rng.random() < 0.5:
+            # whatever "auto" picks (med3 / oblivious / select / data-aware)
+            kw = int(rng.integers(1, 14)) * 2 + 1
+            kh = kw if rng.random() < 0.7 else int(rng.integers(1, 14)) * 2 + 1
+            kernel = None
+        elif kw * kh < 81:
             continue
         h = int(rng.integers(1, 400))
         w = int(rng.integers(1, 400))
         kind, img = draw_image(rng, bits, h, w)
-        kernel = "histogram" if bits == 8 else "rank"
         state["case"] = (bits, kw, kh, h, w, kind, n)
         state["t"] = time.time()
         out = run(img, bits, kw, kh, kernel)
