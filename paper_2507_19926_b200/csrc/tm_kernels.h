@@ -23,6 +23,9 @@ int launch_hist8_rect(const Job& job, int kw, int kh, cudaStream_t s);
 bool rank_supports(int bits, int k);
 int launch_rank(int bits, const Job& job, int k, cudaStream_t s);
 bool rank_rect_supports(int bits, int kw, int kh);
+// stream-ordered scratch for the rank kernel (private pool per device; NULL on failure)
+void* rank_stage_alloc(size_t bytes, cudaStream_t s);
+void rank_stage_free(void* p, cudaStream_t s);
 int launch_rank_rect(int bits, const Job& job, int kw, int kh, cudaStream_t s);
 int launch_med3(int bits, const Job& job, cudaStream_t s);
 

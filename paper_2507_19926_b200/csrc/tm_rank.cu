@@ -2,6 +2,8 @@
 // lives in tm_rank.cuh, its instantiations in tm_rank_{u16,u32}_{0..3}.cu.
 #include <cuda_runtime.h>
 
+#include <mutex>
+
 #include "tm_common.cuh"
 #include "tm_kernels.h"
 
@@ -72,6 +74,48 @@ int launch_rank_rect(int bits, const Job& job, int kw, int kh, cudaStream_t s) {
     default: return launch_rank_rect_u32_3(kw, kh, job, s);
   }
 }
+
+// The rank kernel's candidate staging comes from a private stream-ordered
+// pool per device: freed blocks stay reserved between launches (up to 2 GB)
+// without touching the device's default pool, which other users of
+// cudaMallocAsync in the process (e.g. PyTorch) rely on.
+namespace {
+cudaMemPool_t stage_pool() {
+  constexpr int kMaxDev = 64;
+  constexpr uint64_t kKeepBytes = 2ull << 30;
+  static std::mutex mu;
+  static cudaMemPool_t pools[kMaxDev] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return nullptr;
+  std::lock_guard<std::mutex> g(mu);
+  if (!pools[dev]) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    if (cudaMemPoolCreate(&pools[dev], &props) != cudaSuccess) {
+      cudaGetLastError();
+      pools[dev] = nullptr;
+      return nullptr;
+    }
+    uint64_t thr = kKeepBytes;
+    cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  return pools[dev];
+}
+}  // namespace
+
+void* rank_stage_alloc(size_t bytes, cudaStream_t s) {
+  cudaMemPool_t pool = stage_pool();
+  void* p = nullptr;
+  if (!pool || cudaMallocFromPoolAsync(&p, bytes, pool, s) != cudaSuccess) {
+    cudaGetLastError();  // no staging: the kernel places each group with its own scan
+    return nullptr;
+  }
+  return p;
+}
+
+void rank_stage_free(void* p, cudaStream_t s) { cudaFreeAsync(p, s); }
 
 bool rank_supports(int bits, int k) {
   return (bits == 16 || bits == 32) && k >= 3 && k <= 75 && (k & 1);

@@ -142,7 +142,8 @@ static __device__ unsigned long long g_rank_prof[8];  // per translation unit; t
 // build rows, the row test of a candidate and the median rank.
 template <typename T, int K, bool RT>
 __global__ void __launch_bounds__(32, 1)
-    rank_kernel(Job job, int R, int n_strips, int n_segs, int kh_rt) {
+    rank_kernel(Job job, int R, int n_strips, int n_segs, int kh_rt, uint8_t* gstage,
+                int64_t gstride, int gcap) {
   using C = RankCfg<T, K>;
   using SW = typename C::SW;
   constexpr int NB = C::NB;
@@ -159,6 +160,9 @@ __global__ void __launch_bounds__(32, 1)
   int* start = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(cpos) + C::kPosBytes);
   uint32_t* stk = reinterpret_cast<uint32_t*>(start + NB + 1);          // interval stack
   int* cur = reinterpret_cast<int*>(smem);  // placement cursors: idle histogram words
+  // this warp's global staging of spread candidates (gcap entries), or none
+  T* gval = gstage ? reinterpret_cast<T*>(gstage + (int64_t)blockIdx.x * gstride) : nullptr;
+  uint16_t* gpos = gstage ? reinterpret_cast<uint16_t*>(gval + gcap) : nullptr;
   SW sw;
   sw.init(smem, lane, (K * KH + 1) / 2);
   const int W = job.width, SH = job.src_h, CH = job.channels;
@@ -357,18 +361,29 @@ __global__ void __launch_bounds__(32, 1)
       // sweep; stores every pixel whose median lies in those buckets -- its
       // walk ends in bucket b with residual rank R2 - #keys < b, and the median
       // is that rank among b's in-window candidates in sorted order.
-      auto resolve = [&](const auto& kf, int ba, int bb) {
+      // Candidates of buckets [ba, bb] of `kf` into cval / cpos: `from_global`
+      // copies them from the item's global staging (placed there by one scan
+      // for every bucket, below), else one placement scan of the footprint.
+      auto resolve = [&](const auto& kf, int ba, int bb, bool from_global = false) {
         const int base = start[ba];
-        for (int b = ba + lane; b <= bb; b += 32) cur[b] = start[b] - base;
-        __syncwarp();
-        scan([&](uint32_t v, uint32_t p) {
-          const int b = kf(v);
-          if (b >= ba && b <= bb) {
-            const int slot = atomicAdd(&cur[b], 1);
-            cval[slot] = (T)v;
-            cpos[slot] = (uint16_t)p;
+        if (from_global) {
+          const int n = start[bb + 1] - base;
+          for (int i = lane; i < n; i += 32) {  // contiguous, coalesced
+            cval[i] = gval[base + i];
+            cpos[i] = gpos[base + i];
           }
-        });
+        } else {
+          for (int b = ba + lane; b <= bb; b += 32) cur[b] = start[b] - base;
+          __syncwarp();
+          scan([&](uint32_t v, uint32_t p) {
+            const int b = kf(v);
+            if (b >= ba && b <= bb) {
+              const int slot = atomicAdd(&cur[b], 1);
+              cval[slot] = (T)v;
+              cpos[slot] = (uint16_t)p;
+            }
+          });
+        }
         __syncwarp();
         RANK_T(2);
         // small buckets: insertion sort, one bucket per lane
@@ -618,7 +633,24 @@ __global__ void __launch_bounds__(32, 1)
           continue;
         }
         // dense spread candidates: groups of consecutive buckets that fit,
-        // one fine sweep each
+        // one fine sweep each.  With a global staging area every candidate is
+        // placed once (one footprint scan) and each group copies its
+        // contiguous bucket range into shared memory, instead of one
+        // placement scan of the whole footprint per group.
+        const bool staged = gval != nullptr;
+        if (staged) {
+          for (int b = lane; b < NB; b += 32) cur[b] = start[b];
+          __syncwarp();
+          scan([&](uint32_t v, uint32_t p) {
+            const int b = kf(v);
+            if (b >= 1 && b <= NB - 2) {
+              const int slot = atomicAdd(&cur[b], 1);
+              gval[slot] = (T)v;
+              gpos[slot] = (uint16_t)p;
+            }
+          });
+          __syncwarp();
+        }
         for (int b = 1; b <= NB - 2;) {
           const int cb = start[b + 1] - start[b];
           if (cb > C::CMAX) {
@@ -634,7 +666,7 @@ __global__ void __launch_bounds__(32, 1)
           }
           int e = b;
           while (e + 1 <= NB - 2 && start[e + 2] - start[b] <= C::CMAX) e++;
-          if (start[e + 1] > start[b]) resolve(kf, b, e);
+          if (start[e + 1] > start[b]) resolve(kf, b, e, staged);
           b = e + 1;
         }
       }
@@ -682,8 +714,16 @@ int launch_rank_k(const Job& job, cudaStream_t stream, int kh = K) {
   const int n_segs = (job.out_h + R - 1) / R;
   const long items = (long)n_segs * n_strips * job.channels;
   const int grid = (int)(items < slots ? items : slots);
-  fn<<<grid, 32, kSmem, stream>>>(job, R, n_strips, n_segs, kh);
-  return (int)cudaGetLastError();
+  // global staging for spread candidates: one footprint's worth per resident
+  // warp, stream-ordered from a private pool (kernel falls back to one
+  // placement scan per group when the allocation fails)
+  const int gcap = C::FW * (R + kh - 1);
+  const int64_t gstride = (((int64_t)gcap * (int64_t)(sizeof(T) + 2)) + 255) / 256 * 256;
+  uint8_t* gstage = static_cast<uint8_t*>(rank_stage_alloc((size_t)gstride * grid, stream));
+  fn<<<grid, 32, kSmem, stream>>>(job, R, n_strips, n_segs, kh, gstage, gstride, gcap);
+  const int err = (int)cudaGetLastError();
+  if (gstage) rank_stage_free(gstage, stream);
+  return err;
 }
 
 }  // namespace
