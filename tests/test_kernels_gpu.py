@@ -96,6 +96,22 @@ def test_histogram_u8_wide_short_image_pieces_span_strips():
         assert np.array_equal(run_forced("histogram", img, k), oracle_median_filter_c(img, k)), k
 
 
+@pytest.mark.parametrize("ch", [2, 4, 5])
+def test_histogram_u8_continuous_pieces_channels(ch):
+    """Large interleaved images take the equal-piece split with groups of
+    (adjacent strips x channels) warps; 2, 4 and 5 channels give different
+    group shapes (5: one strip per group) and partial last strip blocks."""
+    from oracle import banded_oracle
+    rng = np.random.default_rng(ch)
+    img = rng.integers(0, 256, (4480, 6720, ch), dtype=np.uint8)  # the C2 frame size
+    out = run_forced("histogram", img, 17)
+    for c in range(ch):
+        plane = np.ascontiguousarray(img[..., c])
+        for y0 in (0, 1100, 2239, 4480 - 48):  # edges and piece / strip boundaries
+            ref = banded_oracle(plane, 17, y0, y0 + 48)
+            assert np.array_equal(out[y0:y0 + 48, :, c], ref), (ch, c, y0)
+
+
 RANK_KS = [3, 9, 17, 29, 33, 47, 75]
 
 
