@@ -1,11 +1,13 @@
 // tm_sweep.cuh -- the warp-level sliding-histogram sweep shared by the data-
-// aware kernels (tm_hist.cu: 8-bit samples, NB = 256 bins; tm_rank.cu: 7-bit
+// aware kernels (tm_hist.cuh: 8-bit samples, NB = 256 bins; tm_rank.cuh: 7-bit
 // keys derived from 16/32-bit samples, NB = 128).
 //
 // One warp owns 32*CPL adjacent output columns; lane l owns columns CPL*l ..
 // CPL*l + CPL-1, whose NB-bin histograms share storage: bin v of the lane's
-// column c is bit field c (16 bits for CPL = 2, 10 bits for CPL = 3 when
-// K^2 <= 1023) of one 32-bit word.  A key at window column j (0..K+CPL-2
+// column c is bit field c (16 bits for CPL = 2, 10 bits for CPL = 3 when the
+// window holds fewer than 512 samples) of one 32-bit word.  The window is K
+// columns wide; its height only enters through the median rank (r2, set at
+// init: (K * k_h + 1) / 2), so rectangular windows share the code.  A key at window column j (0..K+CPL-2
 // relative to the lane's first column) belongs to column c's window when
 // c <= j < c + K, so its update is ONE shared-memory atomic add of a
 // compile-time constant (e.g. 0x1 / 0x10001 / 0x10000 for CPL = 2) -- RED.ADD:
@@ -16,11 +18,12 @@
 // x 32 lanes, word (bin, lane) at bin * 32 + lane -- a warp's accesses hit 32
 // distinct banks whatever the bins.
 //
-// Median tracking per column: m = bin holding rank R2, bl = #keys < m.  A row
-// step applies the leaving and entering rows, updates bl with SIMD byte
-// compares (__vsetltu4: 4 keys per instruction) and walks m up to 8 bins per
-// round trip; the walk is warp-convergent (a converged lane's step is
-// idempotent, so the lanes loop until all agree).
+// Median tracking per column: m = bin holding rank r2, bl = #keys < m.  A row
+// step applies the leaving and entering rows, updates bl with guard-bit-free
+// SIMD byte compares (4 keys per IADD + LOP3 + dp4a) and walks m up to 8 bins
+// per round trip for all CPL columns at once (packed-field arithmetic); the
+// walk is warp-convergent (a converged lane's step is idempotent, so the lanes
+// loop until all agree) and its per-column update is branch-free.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
