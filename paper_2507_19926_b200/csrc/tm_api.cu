@@ -77,11 +77,13 @@ int aware_kernel(int bits, int k) {
 
 // "auto": the fastest exact kernel per (bits, k), measured on B200 over the
 // full k = 3..75 sweep of 4096^2 images (profiles/r01_sweep_4096_all_kernels
-// .jsonl): the oblivious network up to the crossover, the data-aware kernel
-// from it on.  Crossovers: 8-bit k = 15, 16-bit k = 27, 32-bit k = 23.
+// .jsonl, re-measured in round 2 around the crossovers): the oblivious network
+// up to the crossover, the data-aware kernel from it on.  Crossovers: 8-bit
+// k = 13 (round 2: histogram 64.0 vs network 62.5 Gpx/s at 4096^2, 68.7 vs
+// 64.4 at 8192^2), 16-bit k = 27, 32-bit k = 23.
 int auto_kernel(int bits, int k) {
   if (k == 3) return TM_KERNEL_MED3;
-  const int crossover = bits == 8 ? 15 : (bits == 16 ? 27 : 23);
+  const int crossover = bits == 8 ? 13 : (bits == 16 ? 27 : 23);
   if (k < crossover && find_obl(bits, k)) return TM_KERNEL_OBLIVIOUS;
   return aware_kernel(bits, k);
 }

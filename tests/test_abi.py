@@ -49,7 +49,7 @@ def test_dispatch_table_crossovers():
     """auto: oblivious below the measured crossover, data-aware from it on."""
     lib = _lib.load()
     name = lambda b, k, v=0: lib.tm_kernel_name(lib.tm_dispatch_query(b, k, k, v)).decode()
-    assert [name(8, k) for k in (13, 15, 75)] == ["oblivious", "histogram", "histogram"]
+    assert [name(8, k) for k in (11, 13, 75)] == ["oblivious", "histogram", "histogram"]
     assert [name(16, k) for k in (25, 27, 75)] == ["oblivious", "rank", "rank"]
     assert [name(32, k) for k in (21, 23, 75)] == ["oblivious", "rank", "rank"]
     assert name(8, 9, 2) == "histogram" and name(16, 9, 2) == "rank"   # variant "aware"
