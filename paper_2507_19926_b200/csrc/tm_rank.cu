@@ -118,7 +118,9 @@ void* rank_stage_alloc(size_t bytes, cudaStream_t s) {
 void rank_stage_free(void* p, cudaStream_t s) { cudaFreeAsync(p, s); }
 
 bool rank_supports(int bits, int k) {
-  return (bits == 16 || bits == 32) && k >= 3 && k <= 75 && (k & 1);
+  // k <= 127: footprint rows (R + k - 1 <= 254) and columns (64 + k - 1)
+  // stay below 256 in the candidates' 16-bit positions
+  return (bits == 16 || bits == 32) && k >= 3 && k <= 127 && (k & 1);
 }
 
 int launch_rank(int bits, const Job& job, int k, cudaStream_t s) {

@@ -1,5 +1,6 @@
 // tm_rank_u16_0.cu -- instantiations of the rank kernel (tm_rank.cuh) for
-// u16 and k in {3, 11, 19, 27, 35, 43, 51, 59, 67, 75} (split so the build compiles in parallel).
+// u16 and k in {3, 11, 19, 27, 35, 43, 51, 59, 67, 75, 83, 91, 99, 107, 115, 123}
+// (split so the build compiles in parallel).
 #include "tm_rank.cuh"
 
 namespace tmb {
@@ -16,6 +17,12 @@ int launch_rank_u16_0(int k, const Job& job, cudaStream_t s) {
     case 59: return launch_rank_k<uint16_t, 59>(job, s);
     case 67: return launch_rank_k<uint16_t, 67>(job, s);
     case 75: return launch_rank_k<uint16_t, 75>(job, s);
+    case 83: return launch_rank_k<uint16_t, 83>(job, s);
+    case 91: return launch_rank_k<uint16_t, 91>(job, s);
+    case 99: return launch_rank_k<uint16_t, 99>(job, s);
+    case 107: return launch_rank_k<uint16_t, 107>(job, s);
+    case 115: return launch_rank_k<uint16_t, 115>(job, s);
+    case 123: return launch_rank_k<uint16_t, 123>(job, s);
     default: return (int)cudaErrorInvalidValue;
   }
 }

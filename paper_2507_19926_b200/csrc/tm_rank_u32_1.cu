@@ -1,5 +1,6 @@
 // tm_rank_u32_1.cu -- instantiations of the rank kernel (tm_rank.cuh) for
-// u32 and k in {5, 13, 21, 29, 37, 45, 53, 61, 69} (split so the build compiles in parallel).
+// u32 and k in {5, 13, 21, 29, 37, 45, 53, 61, 69, 77, 85, 93, 101, 109, 117, 125}
+// (split so the build compiles in parallel).
 #include "tm_rank.cuh"
 
 namespace tmb {
@@ -15,6 +16,13 @@ int launch_rank_u32_1(int k, const Job& job, cudaStream_t s) {
     case 53: return launch_rank_k<uint32_t, 53>(job, s);
     case 61: return launch_rank_k<uint32_t, 61>(job, s);
     case 69: return launch_rank_k<uint32_t, 69>(job, s);
+    case 77: return launch_rank_k<uint32_t, 77>(job, s);
+    case 85: return launch_rank_k<uint32_t, 85>(job, s);
+    case 93: return launch_rank_k<uint32_t, 93>(job, s);
+    case 101: return launch_rank_k<uint32_t, 101>(job, s);
+    case 109: return launch_rank_k<uint32_t, 109>(job, s);
+    case 117: return launch_rank_k<uint32_t, 117>(job, s);
+    case 125: return launch_rank_k<uint32_t, 125>(job, s);
     default: return (int)cudaErrorInvalidValue;
   }
 }

@@ -1,5 +1,6 @@
 // tm_rank_u32_2.cu -- instantiations of the rank kernel (tm_rank.cuh) for
-// u32 and k in {7, 15, 23, 31, 39, 47, 55, 63, 71} (split so the build compiles in parallel).
+// u32 and k in {7, 15, 23, 31, 39, 47, 55, 63, 71, 79, 87, 95, 103, 111, 119, 127}
+// (split so the build compiles in parallel).
 #include "tm_rank.cuh"
 
 namespace tmb {
@@ -15,6 +16,13 @@ int launch_rank_u32_2(int k, const Job& job, cudaStream_t s) {
     case 55: return launch_rank_k<uint32_t, 55>(job, s);
     case 63: return launch_rank_k<uint32_t, 63>(job, s);
     case 71: return launch_rank_k<uint32_t, 71>(job, s);
+    case 79: return launch_rank_k<uint32_t, 79>(job, s);
+    case 87: return launch_rank_k<uint32_t, 87>(job, s);
+    case 95: return launch_rank_k<uint32_t, 95>(job, s);
+    case 103: return launch_rank_k<uint32_t, 103>(job, s);
+    case 111: return launch_rank_k<uint32_t, 111>(job, s);
+    case 119: return launch_rank_k<uint32_t, 119>(job, s);
+    case 127: return launch_rank_k<uint32_t, 127>(job, s);
     default: return (int)cudaErrorInvalidValue;
   }
 }

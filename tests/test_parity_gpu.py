@@ -217,9 +217,9 @@ def test_host_entry_point_pipelined_bands(bits, k, shape):
 
 @pytest.mark.parametrize("bits", [8, 16, 32])
 def test_kernels_above_75(bits):
-    """k = 77..127 (beyond the dispatch table's k <= 75): auto / aware run the
-    reference's multi-pass engine on the GPU, oblivious / oracle the per-pixel
-    selection kernel -- all exact."""
+    """k = 77..127: auto / aware run the data-aware sweeps (histogram for
+    8-bit, rank for 16/32-bit), oblivious / oracle the per-pixel selection
+    kernel -- all exact."""
     img = generate(TestImageSpec("random", 90, 70, bits, seed=77))
     for k in (77, 101, 127):
         ref = oracle_median_filter_c(img, k)

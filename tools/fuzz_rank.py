@@ -112,6 +112,8 @@ def main():
         bits = int(rng.choice([8, 16, 16, 32, 32]))
         kw = int(rng.integers(1, 38)) * 2 + 1
         kh = kw if rng.random() < 0.6 else int(rng.integers(1, 64)) * 2 + 1
+        if rng.random() < 0.1:  # square windows beyond 75 (up to the ABI's 127)
+            kw = kh = int(rng.integers(38, 64)) * 2 + 1
         kernel = "histogram" if bits == 8 else "rank"
         if a.all_kernels and rng.random() < 0.5:
             # whatever "auto" picks (med3 / oblivious / select / data-aware)
