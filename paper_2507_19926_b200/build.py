@@ -92,6 +92,10 @@ def build(jobs: int | None = None, force: bool = False, verbose: bool = False) -
             stale = any(not os.path.exists(d) or os.path.getmtime(d) > t_obj for d in deps)
         if stale:
             todo.append(src)
+    # the template-heavy data-aware kernels compile longest: start them first so
+    # the many small generated files fill the other cores meanwhile
+    heavy = ("tm_rank", "tm_hist", "tm_aware", "tm_select")
+    todo.sort(key=lambda src: 0 if os.path.basename(src).startswith(heavy) else 1)
     logs = {}
     if todo:
         jobs = jobs or min(len(todo), os.cpu_count() or 4)

@@ -150,29 +150,57 @@ struct WarpSweep {
     // (no borrow across bytes); a < t iff bit 7 of MAJ(~a, t, ~d).  The bytes
     // of the column's window are summed with dp4a (weights = the window mask),
     // 128 per key below the threshold.
-    uint32_t a_in[NC], a_out[NC];
-#pragma unroll
-    for (int i = 0; i < NC; i++) {
-      a_in[i] = ci[i] & 0x7F7F7F7Fu;
-      a_out[i] = co[i] & 0x7F7F7F7Fu;
-    }
-#pragma unroll
-    for (int c = 0; c < CPL; c++) {
-      const uint32_t tb = (uint32_t)m[c] * 0x01010101u;
-      const uint32_t cb = 0x80808080u - (tb & 0x7F7F7F7Fu);
-      int acc_i = 0, acc_o = 0;
+    if constexpr (NB <= 128) {
+      // 7-bit keys (the rank kernel): bit 7 of every byte is free, so
+      // (a | 0x80) - t never borrows across bytes and its bit 7 is [a >= t];
+      // the guard word is shared by every column
+      uint32_t g_in[NC], g_out[NC];
 #pragma unroll
       for (int i = 0; i < NC; i++) {
-        const uint32_t mk = mask(c, i);
-        if (mk) {
-          const uint32_t di = a_in[i] + cb, dout = a_out[i] + cb;
-          const uint32_t li = ((~ci[i] & tb) | (~ci[i] & ~di) | (tb & ~di)) & 0x80808080u;
-          const uint32_t lo = ((~co[i] & tb) | (~co[i] & ~dout) | (tb & ~dout)) & 0x80808080u;
-          acc_i = (int)__dp4a(li, mk, (unsigned)acc_i);
-          acc_o = (int)__dp4a(lo, mk, (unsigned)acc_o);
-        }
+        g_in[i] = ci[i] | 0x80808080u;
+        g_out[i] = co[i] | 0x80808080u;
       }
-      bl[c] += (acc_i - acc_o) >> 7;
+#pragma unroll
+      for (int c = 0; c < CPL; c++) {
+        const uint32_t tb = (uint32_t)m[c] * 0x01010101u;  // m <= 127 + kPad < 256
+        int acc_i = 0, acc_o = 0;
+#pragma unroll
+        for (int i = 0; i < NC; i++) {
+          const uint32_t mk = mask(c, i);
+          if (mk) {
+            const uint32_t li = ~(g_in[i] - tb) & 0x80808080u;
+            const uint32_t lo = ~(g_out[i] - tb) & 0x80808080u;
+            acc_i = (int)__dp4a(li, mk, (unsigned)acc_i);
+            acc_o = (int)__dp4a(lo, mk, (unsigned)acc_o);
+          }
+        }
+        bl[c] += (acc_i - acc_o) >> 7;
+      }
+    } else {
+      uint32_t a_in[NC], a_out[NC];
+#pragma unroll
+      for (int i = 0; i < NC; i++) {
+        a_in[i] = ci[i] & 0x7F7F7F7Fu;
+        a_out[i] = co[i] & 0x7F7F7F7Fu;
+      }
+#pragma unroll
+      for (int c = 0; c < CPL; c++) {
+        const uint32_t tb = (uint32_t)m[c] * 0x01010101u;
+        const uint32_t cb = 0x80808080u - (tb & 0x7F7F7F7Fu);
+        int acc_i = 0, acc_o = 0;
+#pragma unroll
+        for (int i = 0; i < NC; i++) {
+          const uint32_t mk = mask(c, i);
+          if (mk) {
+            const uint32_t di = a_in[i] + cb, dout = a_out[i] + cb;
+            const uint32_t li = ((~ci[i] & tb) | (~ci[i] & ~di) | (tb & ~di)) & 0x80808080u;
+            const uint32_t lo = ((~co[i] & tb) | (~co[i] & ~dout) | (tb & ~dout)) & 0x80808080u;
+            acc_i = (int)__dp4a(li, mk, (unsigned)acc_i);
+            acc_o = (int)__dp4a(lo, mk, (unsigned)acc_o);
+          }
+        }
+        bl[c] += (acc_i - acc_o) >> 7;
+      }
     }
     walk();
   }
